@@ -1,0 +1,439 @@
+/*
+ * fabf_oracle.c -- CPU ORACLE for the fast adaptive bilateral filter of
+ * Gavaskar & Chaudhury, "Fast Adaptive Bilateral Filtering", arXiv 1811.02308.
+ *
+ * THIS FILE IS TEST INFRASTRUCTURE, NOT PRODUCT CODE.
+ *   Only tests/, __graft_entry__.smoke() and bench.py (its cpu_baseline leg and
+ *   `--impl reference`) may load, call or execute it.  It shares no code, no
+ *   header, no table and no constant generator with the CUDA path under
+ *   paper_1811_02308_b200/csrc; neither side includes or links the other.
+ *
+ * Citations: "P:<n>" is a line of /root/reference/PAPER.md (the paper's LaTeX);
+ * equation numbers are the paper's as compiled.
+ *
+ * What it computes (plain, slow, obviously correct):
+ *   fabfo_bounds   alpha_i = min, beta_i = max over the window   eq.(8)
+ *   fabfo_brute    the adaptive bilateral filter g by brute force eq.(1)-(3)
+ *                  P:54-67, with a box spatial kernel (reading R1)
+ *   fabfo_fast     the paper's approximation g-hat of eq.(29), per
+ *                  pixel, evaluated in __float128:
+ *                    mu_k  = sum_{t in Gamma_i} t^k H_i(t)      eq.(22)
+ *                            (the stretched moments, summed directly over the
+ *                            window; Prop.3 / eq.(24) is checked against this in
+ *                            tests, it is not needed to *define* mu)
+ *                    c     = A^{-1} mu, A^{-1} by Theorem 1     eq.(19)
+ *                    lambda, theta_0                           eq.(25)
+ *                    I_0..I_{N+1}                              eq.(28)
+ *                            by eq.(31) (two erf), eq.(32), and the recursion
+ *                            eq.(30); where eq.(30) is numerically
+ *                            unusable (small lambda, reading R9) the
+ *                            integral of eq.(28) is evaluated by 64-node
+ *                            Gauss-Legendre quadrature instead (its definition).
+ *                    g-hat = alpha + (beta-alpha) (sum c_k I_{k+1})/(sum c_k I_k)
+ *                                                                eq.(29)
+ *                  plus the guard of DESIGN.md reading R7 (T2 <= 0 or kappa > 1e3
+ *                  -> the paper's own N=0 value alpha+(beta-alpha) I_1/I_0).
+ *
+ * Border handling (the paper is silent): half-sample symmetric reflection,
+ * DESIGN.md reading R2.  Window: box of half-width rho, (2rho+1)^2 samples,
+ * omega == 1 (reading R1; the paper allows any kernel).
+ *
+ * Precision: every step of fabfo_fast is carried in __float128 (113-bit
+ * mantissa) and rounded once to double at the end (reading R6).  fabfo_brute
+ * is fp64 with the exponent shifted by the window's smallest (f-theta)^2 so no
+ * weight underflows; the ratio eq.(1)/(2) is unchanged by that common factor.
+ *
+ * Pins (tests/test_oracle_*.py, marker "not gpu"): Hilbert inverse against the
+ * exact rational inverse; moment matching residuals; eq.(24) against direct
+ * stretched moments; integrals against mpmath quadrature and closed forms;
+ * g-hat against an independent projection-identity evaluation; limits
+ * (constant window, sigma -> inf, rho = 0); brute force against an independent
+ * numpy implementation and its limits.  Nothing here is "parity unpinned".
+ */
+#include <math.h>
+#include <quadmath.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef __float128 qd;
+
+#define FABFO_MAX_N 16
+#define FABFO_GL_NODES 64
+#define FABFO_KAPPA_MAX 1000.0
+
+/* output code bits (mirrors the meaning documented in DESIGN.md) */
+#define FABFO_CODE_IDENTITY 1u /* alpha == beta -> g-hat = f(i) */
+#define FABFO_CODE_GUARD 2u    /* guard of reading R7 fired                      */
+#define FABFO_CODE_QUAD 4u     /* I_k by quadrature (small lambda), not eq.(30)  */
+
+/* ------------------------------------------------------------------------- */
+/* borders: half-sample symmetric reflection (reading R2); one fold suffices   */
+/* because the caller guarantees 2*rho+1 <= min(H, W).                         */
+static long reflect_index(long i, long n) {
+  if (i < 0) return -i - 1;
+  if (i >= n) return 2 * n - 1 - i;
+  return i;
+}
+
+/* gather the (2rho+1)^2 window of pixel (b, y, x) into vals[] */
+static int gather_window(const float* img, int H, int W, int rho, long b, long y,
+                         long x, float* vals) {
+  const float* base = img + b * (long)H * (long)W;
+  int n = 0;
+  for (long dy = -rho; dy <= rho; ++dy) {
+    long yy = reflect_index(y + dy, H);
+    for (long dx = -rho; dx <= rho; ++dx) {
+      long xx = reflect_index(x + dx, W);
+      vals[n++] = base[yy * W + xx];
+    }
+  }
+  return n;
+}
+
+/* ------------------------------------------------------------------------- */
+/* eq.(8): alpha_i = min Lambda_i, beta_i = max Lambda_i, by scan    */
+int fabfo_bounds(const float* img, int B, int H, int W, int rho, long p0, long p1,
+                 float* alpha, float* beta) {
+  if (!img || !alpha || !beta || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
+  if (2 * rho + 1 > H || 2 * rho + 1 > W) return 1;
+  long HW = (long)H * W;
+  for (long p = p0; p < p1; ++p) {
+    long b = p / HW, r = p % HW, y = r / W, x = r % W;
+    const float* base = img + b * HW;
+    float mn = INFINITY, mx = -INFINITY;
+    for (long dy = -rho; dy <= rho; ++dy) {
+      long yy = reflect_index(y + dy, H);
+      for (long dx = -rho; dx <= rho; ++dx) {
+        float v = base[yy * W + reflect_index(x + dx, W)];
+        if (v < mn) mn = v;
+        if (v > mx) mx = v;
+      }
+    }
+    alpha[p] = mn;
+    beta[p] = mx;
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* eq.(1)-(3) P:54-67: brute-force adaptive bilateral filter, box omega.       */
+/* phi_i(t) = exp(-t^2 / (2 sigma(i)^2)); weights shifted by the smallest      */
+/* exponent in the window (common factor, cancels in the ratio).               */
+int fabfo_brute(const float* img, const float* theta, const float* sigma, int B,
+                int H, int W, int rho, long p0, long p1, double* g) {
+  if (!img || !theta || !sigma || !g || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
+  if (2 * rho + 1 > H || 2 * rho + 1 > W) return 1;
+  long HW = (long)H * W;
+  int n = (2 * rho + 1) * (2 * rho + 1);
+  float* vals = (float*)malloc(sizeof(float) * (size_t)n);
+  if (!vals) return 2;
+  for (long p = p0; p < p1; ++p) {
+    long b = p / HW, r = p % HW, y = r / W, x = r % W;
+    gather_window(img, H, W, rho, b, y, x, vals);
+    double th = theta[p], s = sigma[p];
+    double inv2s2 = 1.0 / (2.0 * s * s);
+    double emin = INFINITY;
+    for (int j = 0; j < n; ++j) {
+      double e = ((double)vals[j] - th) * ((double)vals[j] - th) * inv2s2;
+      if (e < emin) emin = e;
+    }
+    double num = 0.0, den = 0.0;
+    for (int j = 0; j < n; ++j) {
+      double e = ((double)vals[j] - th) * ((double)vals[j] - th) * inv2s2;
+      double w = exp(-(e - emin)); /* omega(j) = 1 (box) */
+      num += w * (double)vals[j];
+      den += w;
+    }
+    g[p] = num / den;
+  }
+  free(vals);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* exact integer binomial coefficient (small arguments only)                   */
+static qd binom_q(int n, int k) {
+  if (k < 0 || k > n) return 0;
+  unsigned __int128 c = 1;
+  for (int i = 1; i <= k; ++i) c = c * (unsigned)(n - k + i) / (unsigned)i;
+  return (qd)c;
+}
+
+/* Theorem 1, eq.(19) P:290-299, 1-based indices m, n = 1..N+1:                */
+/* (A^{-1})_{mn} = (-1)^{m+n} (m+n-1) C(N+m, N+1-n) C(N+n, N+1-m) C(m+n-2,m-1)^2 */
+static qd hilbert_inv_entry(int N, int m, int n) {
+  qd b3 = binom_q(m + n - 2, m - 1);
+  qd v = (qd)(m + n - 1) * binom_q(N + m, N + 1 - n) * binom_q(N + n, N + 1 - m) * b3 * b3;
+  return ((m + n) % 2) ? -v : v;
+}
+
+int fabfo_hilbert_inverse(int N, double* out) {
+  if (N < 0 || N > FABFO_MAX_N || !out) return 1;
+  for (int m = 1; m <= N + 1; ++m)
+    for (int n = 1; n <= N + 1; ++n)
+      out[(m - 1) * (N + 1) + (n - 1)] = (double)hilbert_inv_entry(N, m, n);
+  return 0;
+}
+
+/* c = A^{-1} mu (Algorithm 1 line 11), in __float128 */
+static void fit_q(const qd* mu, int N, qd* c) {
+  for (int m = 1; m <= N + 1; ++m) {
+    qd s = 0;
+    for (int n = 1; n <= N + 1; ++n) s += hilbert_inv_entry(N, m, n) * mu[n - 1];
+    c[m - 1] = s;
+  }
+}
+
+int fabfo_fit(const double* mu, int N, double* c) {
+  if (N < 0 || N > FABFO_MAX_N || !mu || !c) return 1;
+  qd muq[FABFO_MAX_N + 1], cq[FABFO_MAX_N + 1];
+  for (int k = 0; k <= N; ++k) muq[k] = mu[k];
+  fit_q(muq, N, cq);
+  for (int k = 0; k <= N; ++k) c[k] = (double)cq[k];
+  return 0;
+}
+
+/* Prop.3, eq.(24): mu_k = (beta-alpha)^{-k} sum_r C(k,r)(-alpha)^{k-r} m_r */
+int fabfo_stretch(const double* m, int N, double alpha, double beta, double* mu) {
+  if (N < 0 || N > FABFO_MAX_N || !m || !mu || !(beta > alpha)) return 1;
+  qd a = alpha, d = (qd)beta - (qd)alpha;
+  for (int k = 0; k <= N; ++k) {
+    qd s = 0;
+    for (int r = 0; r <= k; ++r) {
+      qd pw = 1;
+      for (int e = 0; e < k - r; ++e) pw *= -a;
+      s += binom_q(k, r) * pw * (qd)m[r];
+    }
+    qd dk = 1;
+    for (int e = 0; e < k; ++e) dk *= d;
+    mu[k] = (double)(s / dk);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 64-node Gauss-Legendre rule on [0,1] in __float128 (library-primitive use:  */
+/* numerical quadrature of the integral that eq.(28) defines).                 */
+static qd gl_x[FABFO_GL_NODES], gl_w[FABFO_GL_NODES];
+
+__attribute__((constructor)) static void gl_init(void) {
+  const int n = FABFO_GL_NODES;
+  for (int i = 0; i < n; ++i) {
+    qd x = cosq(M_PIq * ((qd)i + 0.75Q) / ((qd)n + 0.5Q));
+    qd dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      qd p0 = 1, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        qd p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1);
+      qd dx = p1 / dp;
+      x -= dx;
+      if (fabsq(dx) < 1e-40Q) break;
+    }
+    /* recompute derivative at the converged node */
+    {
+      qd p0 = 1, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        qd p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1);
+    }
+    gl_x[i] = (x + 1) / 2;                       /* map [-1,1] -> [0,1] */
+    gl_w[i] = (2 / ((1 - x * x) * dp * dp)) / 2; /* Jacobian 1/2        */
+  }
+}
+
+/* I_k = int_0^1 t^k exp(-lambda (t - t0)^2) dt, k = 0..K   (eq.(28))
+ * method 1: eq.(31) P:432-435 for I_0 (two erf; written with erfc where both
+ *           arguments share a sign so the difference does not cancel), eq.(32)
+ *           P:436-440 for I_1, recursion eq.(30) P:423-426 for k >= 2.
+ * method 2: 64-node Gauss-Legendre quadrature of the eq.(28) integrand.
+ * method 0: automatic -- method 2 where eq.(30)'s forward recursion loses
+ *           precision (lambda <= 1 and a slowly varying integrand, reading R9),
+ *           method 1 otherwise.                                                */
+static int integrals_q(qd lam, qd t0, int K, qd* I, int method) {
+  qd far = fmaxq(fabsq(t0), fabsq(1 - t0));
+  if (method == 0) method = (lam <= 1 && 2 * lam * far <= 24) ? 2 : 1;
+  if (method == 2) {
+    for (int k = 0; k <= K; ++k) I[k] = 0;
+    for (int q = 0; q < FABFO_GL_NODES; ++q) {
+      qd x = gl_x[q];
+      qd e = gl_w[q] * expq(-lam * (x - t0) * (x - t0));
+      qd xp = 1;
+      for (int k = 0; k <= K; ++k) {
+        I[k] += e * xp;
+        xp *= x;
+      }
+    }
+    return 2;
+  }
+  qd sl = sqrtq(lam);
+  qd a = sl * (1 - t0), b = -sl * t0; /* I_0 = 1/2 sqrt(pi/lam) [erf(a) - erf(b)] */
+  qd diff;
+  if (a > 0 && b > 0)
+    diff = erfcq(b) - erfcq(a);
+  else if (a < 0 && b < 0)
+    diff = erfcq(-a) - erfcq(-b);
+  else
+    diff = erfq(a) - erfq(b);
+  qd E0 = expq(-lam * t0 * t0);
+  qd E1 = expq(-lam * (1 - t0) * (1 - t0));
+  I[0] = 0.5Q * sqrtq(M_PIq / lam) * diff;
+  if (K >= 1) I[1] = t0 * I[0] + (E0 - E1) / (2 * lam);
+  for (int k = 2; k <= K; ++k) I[k] = t0 * I[k - 1] + (qd)(k - 1) / (2 * lam) * I[k - 2] - E1 / (2 * lam);
+  return 1;
+}
+
+int fabfo_integrals(double lam, double t0, int K, double* I, int method) {
+  if (!(lam > 0) || K < 0 || K > FABFO_MAX_N + 1 || !I || method < 0 || method > 2) return -1;
+  qd Iq[FABFO_MAX_N + 2];
+  int used = integrals_q(lam, t0, K, Iq, method);
+  for (int k = 0; k <= K; ++k) I[k] = (double)Iq[k];
+  return used;
+}
+
+/* shifted Legendre polynomial coefficients: P~_k(t) = P_k(2t-1)
+ * = sum_r (-1)^{k+r} C(k,r) C(k+r,r) t^r  (used only for the diagnostic kappa
+ * of reading R7 -- the guard's condition number is stated in this basis).      */
+static qd shifted_legendre_coef(int k, int r) {
+  qd v = binom_q(k, r) * binom_q(k + r, r);
+  return ((k + r) % 2) ? -v : v;
+}
+
+/* ------------------------------------------------------------------------- */
+/* the per-pixel result                                                        */
+typedef struct {
+  double g_lit;   /* eq.(29) as printed                                  */
+  double g_guard; /* with the guard of reading R7                        */
+  double kappa;   /* sum_k |(2k+1) nu_k J_k| / T2 (Legendre basis)       */
+  double t2n;     /* T2 / n  (n = window size)                           */
+  double lam;     /* lambda_i, eq.(25)                                   */
+  double t0;      /* theta_0(i)                                          */
+  int code;
+} fabfo_px;
+
+/* Algorithm 1 P:446-477 for one pixel whose window samples are vals[0..n-1]  */
+static void fast_window(const float* vals, int n, float f_center, float theta, float sigma,
+                        int N, fabfo_px* out) {
+  memset(out, 0, sizeof(*out));
+  float amin = vals[0], bmax = vals[0];
+  for (int j = 1; j < n; ++j) {
+    if (vals[j] < amin) amin = vals[j];
+    if (vals[j] > bmax) bmax = vals[j];
+  }
+  if (amin == bmax) { /* lines 4-5 P:454-455: g-hat(i) = f(i) */
+    out->g_lit = out->g_guard = f_center;
+    out->kappa = 1.0;
+    out->t2n = 1.0;
+    out->code = FABFO_CODE_IDENTITY;
+    return;
+  }
+  qd alpha = amin, beta = bmax, d = beta - alpha;
+
+  /* eq.(22): mu_k = sum_{t in Gamma_i} t^k H_i(t) = sum_j ((f_j - alpha)/d)^k */
+  qd mu[FABFO_MAX_N + 1];
+  for (int k = 0; k <= N; ++k) mu[k] = 0;
+  for (int j = 0; j < n; ++j) {
+    qd t = ((qd)vals[j] - alpha) / d, tp = 1;
+    for (int k = 0; k <= N; ++k) {
+      mu[k] += tp;
+      tp *= t;
+    }
+  }
+  /* line 11: c = A^{-1} mu */
+  qd c[FABFO_MAX_N + 1];
+  fit_q(mu, N, c);
+  /* lines 12-13: t0, lambda (eq.(25)) */
+  qd t0 = ((qd)theta - alpha) / d;
+  qd lam = d * d / (2 * (qd)sigma * (qd)sigma);
+  /* line 14 + 18: I_0 .. I_{N+1} */
+  qd I[FABFO_MAX_N + 2];
+  int used = integrals_q(lam, t0, N + 1, I, 0);
+  /* lines 15-20: T1, T2 */
+  qd T1 = 0, T2 = 0;
+  for (int k = 0; k <= N; ++k) {
+    T1 += c[k] * I[k + 1];
+    T2 += c[k] * I[k];
+  }
+  qd g_lit = alpha + d * (T1 / T2); /* line 21, eq.(29) */
+
+  /* diagnostic condition number in the Legendre basis (reading R7) */
+  qd absum = 0;
+  for (int k = 0; k <= N; ++k) {
+    qd nu = 0, J = 0;
+    for (int r = 0; r <= k; ++r) {
+      qd L = shifted_legendre_coef(k, r);
+      nu += L * mu[r];
+      J += L * I[r];
+    }
+    absum += fabsq((qd)(2 * k + 1) * nu * J);
+  }
+  qd kappa = (T2 > 0) ? absum / T2 : (qd)INFINITY;
+  qd g_guard = g_lit;
+  int code = (used == 2) ? FABFO_CODE_QUAD : 0;
+  if (!(T2 > 0) || kappa > (qd)FABFO_KAPPA_MAX) {
+    g_guard = alpha + d * (I[1] / I[0]); /* the paper's N = 0 value */
+    code |= FABFO_CODE_GUARD;
+  }
+  out->g_lit = (double)g_lit;
+  out->g_guard = (double)g_guard;
+  out->kappa = (double)kappa;
+  out->t2n = (double)(T2 / n);
+  out->lam = (double)lam;
+  out->t0 = (double)t0;
+  out->code = code;
+}
+
+/* one window given explicitly: out6 = {g_lit, g_guard, kappa, t2n, lam, t0}   */
+int fabfo_window(const float* vals, int n, float f_center, float theta, float sigma, int N,
+                 double* out6, int* code) {
+  if (!vals || n < 1 || N < 0 || N > FABFO_MAX_N || !out6) return 1;
+  fabfo_px px;
+  fast_window(vals, n, f_center, theta, sigma, N, &px);
+  out6[0] = px.g_lit;
+  out6[1] = px.g_guard;
+  out6[2] = px.kappa;
+  out6[3] = px.t2n;
+  out6[4] = px.lam;
+  out6[5] = px.t0;
+  if (code) *code = px.code;
+  return 0;
+}
+
+/* whole-image (or pixel-list) driver.  Pixels are flat indices into B*H*W.
+ * If idx is NULL the pixels are p0..p1-1, else idx[p0..p1-1].  Any output
+ * pointer may be NULL.  Output arrays are indexed like the pixel list.        */
+int fabfo_fast(const float* img, const float* theta, const float* sigma, int B, int H, int W,
+               int rho, int N, const long* idx, long p0, long p1, double* g_lit,
+               double* g_guard, double* kappa, double* t2n, unsigned char* code) {
+  if (!img || !theta || !sigma || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
+  if (2 * rho + 1 > H || 2 * rho + 1 > W || N < 0 || N > FABFO_MAX_N) return 1;
+  long HW = (long)H * W;
+  int n = (2 * rho + 1) * (2 * rho + 1);
+  float* vals = (float*)malloc(sizeof(float) * (size_t)n);
+  if (!vals) return 2;
+  for (long q = p0; q < p1; ++q) {
+    long p = idx ? idx[q] : q;
+    if (p < 0 || p >= (long)B * HW) {
+      free(vals);
+      return 1;
+    }
+    long b = p / HW, r = p % HW, y = r / W, x = r % W;
+    gather_window(img, H, W, rho, b, y, x, vals);
+    fabfo_px px;
+    fast_window(vals, n, img[p], theta[p], sigma[p], N, &px);
+    if (g_lit) g_lit[q] = px.g_lit;
+    if (g_guard) g_guard[q] = px.g_guard;
+    if (kappa) kappa[q] = px.kappa;
+    if (t2n) t2n[q] = px.t2n;
+    if (code) code[q] = (unsigned char)px.code;
+  }
+  free(vals);
+  return 0;
+}

@@ -1,0 +1,215 @@
+"""ctypes front end of the C oracle ``fabf_oracle.c`` (test infrastructure only).
+
+Every function here is argument marshalling plus a thread pool over pixel ranges;
+all arithmetic is in ``fabf_oracle.c``.  See that file's header for the paper
+passages each routine follows (P:<line> = /root/reference/PAPER.md line).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fabf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CODE_IDENTITY = 1
+CODE_GUARD = 2
+CODE_QUAD = 4
+KAPPA_MAX = 1000.0
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C + libquadmath)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-o", tmp, _SRC, "-lquadmath", "-lm"]
+        )
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            i, l, d = ctypes.c_int, ctypes.c_long, ctypes.c_double
+            lib.fabfo_bounds.argtypes = [P, i, i, i, i, l, l, P, P]
+            lib.fabfo_brute.argtypes = [P, P, P, i, i, i, i, l, l, P]
+            lib.fabfo_fast.argtypes = [P, P, P, i, i, i, i, i, P, l, l, P, P, P, P, P]
+            lib.fabfo_window.argtypes = [P, i, ctypes.c_float, ctypes.c_float, ctypes.c_float, i, P, P]
+            lib.fabfo_hilbert_inverse.argtypes = [i, P]
+            lib.fabfo_fit.argtypes = [P, i, P]
+            lib.fabfo_stretch.argtypes = [P, i, d, d, P]
+            lib.fabfo_integrals.argtypes = [d, d, i, P, i]
+            for fn in ("fabfo_bounds", "fabfo_brute", "fabfo_fast", "fabfo_window",
+                       "fabfo_hilbert_inverse", "fabfo_fit", "fabfo_stretch", "fabfo_integrals"):
+                getattr(lib, fn).restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _as3d(a):
+    a = _f32(a)
+    if a.ndim == 2:
+        a = a[None]
+    if a.ndim != 3:
+        raise ValueError("expected H x W or B x H x W")
+    return a
+
+
+def _parallel(total: int, fn, threads: int | None, chunk: int = 4096):
+    threads = threads or os.cpu_count() or 1
+    ranges = [(s, min(total, s + chunk)) for s in range(0, total, chunk)]
+    if threads <= 1 or len(ranges) <= 1:
+        for r in ranges:
+            fn(*r)
+        return
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for fut in [ex.submit(fn, *r) for r in ranges]:
+            fut.result()
+
+
+def bounds(img, rho: int, threads: int | None = None):
+    """eq.(8) P:199-203 by exhaustive window scan -> (alpha, beta), float32."""
+    lib = _load()
+    f = _as3d(img)
+    B, H, W = f.shape
+    alpha = np.empty_like(f)
+    beta = np.empty_like(f)
+
+    def run(p0, p1):
+        if lib.fabfo_bounds(_ptr(f), B, H, W, rho, p0, p1, _ptr(alpha), _ptr(beta)):
+            raise ValueError("fabfo_bounds: invalid arguments")
+
+    _parallel(f.size, run, threads)
+    shp = np.shape(img)
+    return alpha.reshape(shp), beta.reshape(shp)
+
+
+def brute(img, theta, sigma, rho: int, threads: int | None = None):
+    """eq.(1)-(3) P:54-67, box spatial kernel, fp64 -> g (float64)."""
+    lib = _load()
+    f, th, sg = _as3d(img), _as3d(theta), _as3d(sigma)
+    B, H, W = f.shape
+    g = np.empty(f.shape, np.float64)
+
+    def run(p0, p1):
+        if lib.fabfo_brute(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, p0, p1, _ptr(g)):
+            raise ValueError("fabfo_brute: invalid arguments")
+
+    _parallel(f.size, run, threads, chunk=2048)
+    return g.reshape(np.shape(img))
+
+
+def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None = None):
+    """Algorithm 1 / eq.(29) in __float128.
+
+    Returns a dict of arrays: ``g_lit`` (eq.(29) as printed), ``g_guard`` (with the
+    reading-R7 guard), ``kappa``, ``t2n`` (T2/n) and ``code``.  With ``pixels`` (flat
+    indices into B*H*W) only those pixels are computed and the arrays follow that
+    list; otherwise they have the image's shape.
+    """
+    lib = _load()
+    f, th, sg = _as3d(img), _as3d(theta), _as3d(sigma)
+    B, H, W = f.shape
+    if pixels is not None:
+        idx = np.ascontiguousarray(pixels, dtype=np.int64).ravel()
+        total = idx.size
+    else:
+        idx = None
+        total = f.size
+    out = {
+        "g_lit": np.empty(total, np.float64),
+        "g_guard": np.empty(total, np.float64),
+        "kappa": np.empty(total, np.float64),
+        "t2n": np.empty(total, np.float64),
+        "code": np.empty(total, np.uint8),
+    }
+
+    def run(p0, p1):
+        rc = lib.fabfo_fast(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, N, _ptr(idx), p0, p1,
+                            _ptr(out["g_lit"]), _ptr(out["g_guard"]), _ptr(out["kappa"]),
+                            _ptr(out["t2n"]), _ptr(out["code"]))
+        if rc:
+            raise ValueError("fabfo_fast: invalid arguments")
+
+    n = (2 * rho + 1) ** 2
+    _parallel(total, run, threads, chunk=max(16, min(4096, 400000 // max(1, n * (N + 1)))))
+    if pixels is None:
+        shp = np.shape(img)
+        out = {k: v.reshape(shp) for k, v in out.items()}
+    return out
+
+
+def fast_window(vals, f_center: float, theta: float, sigma: float, N: int):
+    """g-hat for one explicit window (samples ``vals``): dict of scalars."""
+    lib = _load()
+    v = _f32(vals).ravel()
+    o = np.empty(6, np.float64)
+    code = ctypes.c_int(0)
+    if lib.fabfo_window(_ptr(v), v.size, float(f_center), float(theta), float(sigma), N, _ptr(o),
+                        ctypes.byref(code)):
+        raise ValueError("fabfo_window: invalid arguments")
+    return dict(g_lit=o[0], g_guard=o[1], kappa=o[2], t2n=o[3], lam=o[4], t0=o[5], code=code.value)
+
+
+def hilbert_inverse(N: int):
+    """Theorem 1, eq.(19), as a float64 (N+1)x(N+1) array."""
+    lib = _load()
+    o = np.empty((N + 1, N + 1), np.float64)
+    if lib.fabfo_hilbert_inverse(N, _ptr(o)):
+        raise ValueError("N out of range")
+    return o
+
+
+def fit(mu, N: int):
+    """c = A^{-1} mu (Algorithm 1 line 11) evaluated in __float128."""
+    lib = _load()
+    m = np.ascontiguousarray(mu, np.float64)
+    c = np.empty(N + 1, np.float64)
+    if lib.fabfo_fit(_ptr(m), N, _ptr(c)):
+        raise ValueError("bad arguments")
+    return c
+
+
+def stretch(m, N: int, alpha: float, beta: float):
+    """Prop.3 eq.(24) P:338-345 (binomial transform) in __float128."""
+    lib = _load()
+    mm = np.ascontiguousarray(m, np.float64)
+    mu = np.empty(N + 1, np.float64)
+    if lib.fabfo_stretch(_ptr(mm), N, alpha, beta, _ptr(mu)):
+        raise ValueError("bad arguments")
+    return mu
+
+
+def integrals(lam: float, t0: float, K: int, method: int = 0):
+    """I_0..I_K of eq.(28); method 0 auto, 1 eqs.(30)-(32), 2 quadrature.
+
+    Returns (I, method_used)."""
+    lib = _load()
+    o = np.empty(K + 1, np.float64)
+    used = lib.fabfo_integrals(lam, t0, K, _ptr(o), method)
+    if used < 0:
+        raise ValueError("bad arguments")
+    return o, used
