@@ -1,0 +1,285 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the fast adaptive bilateral filter on B200.
+
+Workload (BASELINE.json metric / configs[3]): one 3840x2160 grey frame, box
+window rho=20 (41x41), N=8, sigma ~ U[5,60], theta = f + U[-15,15] (synthetic
+Voronoi-256 + noise sd 20 stand-in for the paper's photographs).
+A "step" is one full pass of the hot path (bounds, moments, fit, integrals,
+ratio, exact-moment fallback) over one frame.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun: every rank filters its own frame (independent
+problems, no data-path collective), timing is the max over ranks (weak
+scaling).  ``--impl reference`` times the CPU oracle (oracle/, __float128
+Algorithm 1) on a bounded pixel sample of the same workload on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpix/s of fast adaptive bilateral filter (4K, rho=20, N=8)"
+CFG = 4
+
+
+def _load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_sample(w, npx: int, seed: int = 0):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(w.img.size, npx, replace=False))
+
+
+def time_oracle(w, npx: int, threads: int | None = None):
+    import oracle
+
+    oracle.build()
+    idx = cpu_sample(w, npx)
+    t = time.perf_counter()
+    oracle.fast(w.img, w.theta, w.sigma, w.rho, w.N, pixels=idx, threads=threads)
+    dt = time.perf_counter() - t
+    return npx / dt / 1e6, dt
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on this host's cores."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import workloads
+
+    w = workloads.config(CFG)
+    cores = os.cpu_count() or 1
+    npx = args.ref_pixels
+    for _ in range(args.warmup):
+        time_oracle(w, max(64, npx // 10))
+    times = []
+    for _ in range(args.steps):
+        _, dt = time_oracle(w, npx)
+        times.append(dt)
+    tot = sum(times)
+    value = args.steps * npx / tot / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpix/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f128", "data": "synthetic",
+        "config": {"workload": w.name, "sample": f"{npx} seeded pixels per step of the 8.29 Mpx frame"},
+        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{npx} seeded pixels of {w.name} per step"},
+        "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_1811_02308_b200 as fb
+    from paper_1811_02308_b200 import build
+
+    build.build()
+    import workloads
+
+    w = workloads.config(CFG)
+    B, H, W = w.shape
+    px = B * H * W
+    img = torch.from_numpy(w.img).to(dev)
+    th = torch.from_numpy(w.theta).to(dev)
+    sg = torch.from_numpy(w.sigma).to(dev)
+    out = torch.empty_like(img)
+    plan = fb.Plan(B, H, W)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        fb.filter(plan, img, th, sg, w.rho, w.N, out=out)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = float(sum(step_ms))
+    fallback = plan.last_fallback_count()
+
+    # per-kernel device times (events recorded between the launches, same stream)
+    stage = np.zeros(4)
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        _, ms4 = fb.filter_profile(plan, img, th, sg, w.rho, w.N, out=out)
+        stage += np.array(ms4)
+    stage /= args.steps
+
+    # end to end through the C ABI with host buffers (pinned), copies inside
+    h_img = torch.from_numpy(w.img).pin_memory()
+    h_th = torch.from_numpy(w.theta).pin_memory()
+    h_sg = torch.from_numpy(w.sigma).pin_memory()
+    h_out = torch.empty_like(h_img).pin_memory()
+    fb.filter_host(plan, h_img, h_th, h_sg, w.rho, w.N, h_out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(e2e_steps):
+        fb.filter_host(plan, h_img, h_th, h_sg, w.rho, w.N, h_out)
+    e2e_s = time.perf_counter() - t0
+
+    tot = torch.tensor([tot_ms, e2e_s], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+    tot_ms, e2e_s = float(tot[0]), float(tot[1])
+    value = ws * px * args.steps / (tot_ms * 1e-3) / 1e6
+    e2e_value = ws * px * e2e_steps / e2e_s / 1e6
+
+    if rank == 0:
+        peaks, peak_src = _load_peaks()
+        ms = tot_ms / args.steps
+        alg_bytes = 16.0 * px  # f, theta, sigma read + g written, fp32
+        hbm = {"bound": "hbm", "achieved": alg_bytes / (ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+               "unit": "GB/s", "frac": alg_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+               "traffic": None, "peak_source": peak_src}
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": w.name, "height": H, "width": W, "rho": w.rho, "N": w.N,
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "parallelism": f"{ws} independent frames (one per GPU)" if ws > 1 else "1 GPU"},
+            "roofline": hbm,
+            "step_ms": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms)},
+            "fallback_pixels": fallback,
+            "stage_ms": {"bounds_rows": stage[0], "bounds_cols": stage[1], "filter": stage[2],
+                         "fallback": stage[3]},
+            "e2e": {"value": e2e_value, "unit": "Mpix/s", "h2d_bytes_per_step": 12 * px,
+                    "d2h_bytes_per_step": 4 * px},
+            "gpu_launches": 4 * args.steps,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            v, dt = time_oracle(w, args.ref_pixels)
+            line["cpu_baseline"] = {"value": v, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+                                    "sample": f"{args.ref_pixels} seeded pixels of {w.name} ({dt:.1f} s)"}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fabf", choices=["fabf", "reference"])
+    ap.add_argument("--ref-pixels", type=int, default=20000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

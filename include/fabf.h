@@ -1,0 +1,135 @@
+/*
+ * fabf.h -- C ABI of the B200 (sm_100a) fast adaptive bilateral filter.
+ *
+ * Implements the per-pixel pipeline of Algorithm 1 of Gavaskar & Chaudhury,
+ * "Fast Adaptive Bilateral Filtering", arXiv 1811.02308 (P:446-477 of
+ * /root/reference/PAPER.md), with a box spatial kernel of half-width rho
+ * (reading R1):
+ *
+ *   g-hat(i) = alpha_i + (beta_i - alpha_i) * (sum_k c_k I_{k+1}) / (sum_k c_k I_k)   eq.(29)
+ *
+ * where alpha_i / beta_i are the window min / max (eq.(8)), c the
+ * degree-N moment-matching polynomial of the stretched local histogram
+ * (eqs.(14),(19),(24) P:246-345; computed in the equivalent Legendre basis,
+ * DESIGN.md section "Kernels"), and I_k the Gaussian integrals of eq.(28)
+ * (P:382-441).  Pixels with alpha_i == beta_i return f(i) exactly.
+ *
+ * All image arguments are float32, batch x height x width, row-major,
+ * contiguous.  img, theta and sigma share one intensity scale (any scale: the
+ * filter is affine-equivariant, reading R4).  sigma(i) > 0 and finite
+ * inputs are preconditions (unspecified output otherwise).
+ *
+ * Border handling: half-sample symmetric reflection (reading R2),
+ * which needs 2*rho+1 <= min(height, width).
+ *
+ * Errors: every entry point returns a fabf_status_t; no C++ exception crosses
+ * the ABI.  fabf_last_error_message() gives a thread-local detail string.
+ * CUDA errors raised asynchronously by earlier work on the stream surface on a
+ * later call (or on the caller's own synchronisation).
+ *
+ * Threading / ownership: the caller owns every image buffer and the stream;
+ * a plan owns its device workspace.  Use one plan from one stream at a time.
+ */
+#ifndef FABF_H_
+#define FABF_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FABF_VERSION 100 /* 1.0.0 */
+#define FABF_MAX_N 10    /* largest supported polynomial degree N */
+
+typedef enum {
+  FABF_OK = 0,
+  FABF_ERR_INVALID_ARGUMENT = 1, /* null/misaligned pointer, bad size, rho/N out of range, overlap */
+  FABF_ERR_UNSUPPORTED = 2,      /* device is not sm_100 (B200), or N > FABF_MAX_N       */
+  FABF_ERR_CUDA = 3,             /* a CUDA API call or kernel launch failed               */
+  FABF_ERR_OUT_OF_MEMORY = 4     /* device or host allocation failed                      */
+} fabf_status_t;
+
+/* plan flags */
+#define FABF_FLAG_LITERAL 0x1u /* eq.(29) exactly as printed: no guard (reading R7)       */
+#define FABF_FLAG_CLAMP 0x2u   /* clamp g-hat to [alpha_i, beta_i] after the guard (reading R7)    */
+
+/* per-pixel diagnostic code bits (fabf_diag_t.code) */
+#define FABF_CODE_IDENTITY 0x1u /* alpha == beta: g-hat = f(i)                               */
+#define FABF_CODE_GUARD 0x2u    /* guard fired: T2 <= 0 or kappa > 1e3 -> N = 0 value          */
+#define FABF_CODE_SMALL_LAMBDA 0x4u /* lambda < 2: integrals by fixed-node quadrature        */
+#define FABF_CODE_FALLBACK 0x8u /* moments recomputed exactly (centring amplification flag)  */
+#define FABF_CODE_FAR_THETA 0x10u /* theta_0 outside [-1, 2]: adaptive quadrature            */
+
+typedef struct fabf_plan_s* fabf_plan_t;
+
+/* Create a plan for images of shape batch x height x width (all >= 1).
+ * Allocates the plan's device workspace (the list of pixels flagged for the
+ * exact-moment fallback and its counter) on the current device; no allocation
+ * happens later in fabf_filter.  flags: FABF_FLAG_* (0 = guarded, unclamped).
+ * Returns FABF_ERR_UNSUPPORTED when the current device is not compute
+ * capability 10.0 (this library contains sm_100a code only).                  */
+fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, unsigned flags);
+
+/* The filter.  img, theta, sigma, out: DEVICE pointers (float32,
+ * batch*height*width, 16-byte aligned); out must not overlap any input.
+ * rho >= 0 with 2*rho+1 <= min(height, width); 0 <= N <= FABF_MAX_N.
+ * rho == 0 is an exact copy (every window is a single sample).
+ * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous, does
+ * not synchronise and does not read device memory on the host; capturable
+ * into a CUDA graph.                                                           */
+fabf_status_t fabf_filter(fabf_plan_t plan, const float* img, const float* theta,
+                          const float* sigma, int rho, int N, float* out, void* stream);
+
+/* Optional per-pixel diagnostics (device pointers, batch*height*width each;
+ * any member may be NULL).  kappa = sum_k |(2k+1) nu_k J_k| / T2 is the
+ * condition number of the eq.(29) normaliser in the Legendre basis; t2n = T2/n
+ * (n = (2rho+1)^2); code = FABF_CODE_* bits.                                   */
+typedef struct {
+  float* alpha;
+  float* beta;
+  float* kappa;
+  float* t2n;
+  unsigned char* code;
+} fabf_diag_t;
+
+/* fabf_filter plus diagnostics (diag may be NULL: then identical to
+ * fabf_filter).                                                                */
+fabf_status_t fabf_filter_diag(fabf_plan_t plan, const float* img, const float* theta,
+                               const float* sigma, int rho, int N, float* out,
+                               const fabf_diag_t* diag, void* stream);
+
+/* Step a1 alone: alpha = window min, beta = window max (eq.(8)), box
+ * half-width rho, same borders as fabf_filter.  Device pointers as above.      */
+fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* alpha,
+                          float* beta, void* stream);
+
+/* End-to-end convenience: HOST pointers (pinned memory recommended).  Copies
+ * the inputs to plan-owned device buffers, runs fabf_filter, copies out back,
+ * all enqueued on stream; synchronises the stream before returning.          */
+fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
+                               const float* sigma, int rho, int N, float* out, void* stream);
+
+/* Number of pixels the last fabf_filter* call on this plan routed to the
+ * exact-moment fallback (synchronises the plan's stream to read it).         */
+fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count);
+
+/* Profiling variant of fabf_filter: same work on the same stream, with CUDA
+ * events recorded between the kernels; synchronises the stream and writes the
+ * device time (ms) of each stage to stage_ms[0..3] = {bounds rows pass, bounds
+ * columns pass, moments + per-pixel filter, exact-moment fallback}.           */
+fabf_status_t fabf_filter_profile(fabf_plan_t plan, const float* img, const float* theta,
+                                  const float* sigma, int rho, int N, float* out, void* stream,
+                                  float stage_ms[4]);
+
+/* Free the plan (NULL is a no-op).  No work using the plan may be pending.   */
+fabf_status_t fabf_destroy(fabf_plan_t plan);
+
+const char* fabf_status_string(fabf_status_t status);
+const char* fabf_last_error_message(void);
+int fabf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FABF_H_ */

@@ -1,0 +1,28 @@
+"""B200-native fast adaptive bilateral filter (Gavaskar & Chaudhury, arXiv 1811.02308).
+
+A thin ctypes binding of the C-ABI library ``libfabf.so`` (include/fabf.h): the
+same entry points, argument marshalling only.  Every step of the filter runs in
+the library's sm_100a CUDA kernels; there is no CPU fallback -- importing works
+anywhere, but every call raises if the library or a B200 is missing.  PyTorch is
+used only for device memory and streams.
+"""
+from .fabf import (  # noqa: F401
+    FabfError,
+    Plan,
+    bounds,
+    filter,
+    filter_diag,
+    filter_host,
+    filter_profile,
+    lib,
+    library_path,
+    version,
+    FLAG_LITERAL,
+    FLAG_CLAMP,
+    CODE_IDENTITY,
+    CODE_GUARD,
+    CODE_SMALL_LAMBDA,
+    CODE_FALLBACK,
+    CODE_FAR_THETA,
+    MAX_N,
+)

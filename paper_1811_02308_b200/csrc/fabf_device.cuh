@@ -1,0 +1,265 @@
+// fabf_device.cuh -- per-pixel device math of the fast adaptive bilateral
+// filter (arXiv 1811.02308) for sm_100a.  Included by fabf.cu only.
+//
+// P:<n> = line of /root/reference/PAPER.md.  The stage names follow SURVEY.md
+// section 8(a) (a4 stretch, a5 fit, a6 range parameters, a7 integrals, a8 ratio).
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace fabf {
+
+constexpr int kMaxN = 10;
+constexpr int kGlB = 16;  // fixed-node Gauss-Legendre rule on [0,1], small lambda
+constexpr int kGlC = 24;  // Gauss-Legendre rule on the effective support, far theta_0
+constexpr float kKappaMax = 1000.0f;
+constexpr double kLambdaSmall = 2.0;  // below: fixed-node quadrature (regime B)
+
+// code bits (mirror FABF_CODE_* in include/fabf.h)
+constexpr unsigned kCodeIdentity = 0x1u;
+constexpr unsigned kCodeGuard = 0x2u;
+constexpr unsigned kCodeSmallLambda = 0x4u;
+constexpr unsigned kCodeFallback = 0x8u;
+constexpr unsigned kCodeFarTheta = 0x10u;
+
+// plan flags (mirror FABF_FLAG_*)
+constexpr unsigned kFlagLiteral = 0x1u;
+constexpr unsigned kFlagClamp = 0x2u;
+
+// Legendre polynomial coefficients on [-1,1]: P_k(w) = sum_r leg[k][r] w^r.
+__constant__ double c_leg[kMaxN + 1][kMaxN + 1];
+// Regime B: W[k][q] = w_q * P~_k(x_q), 16-node Gauss-Legendre on [0,1].
+__constant__ float c_glB_x[kGlB];
+__constant__ float c_glB_W[kMaxN + 2][kGlB];
+// Regime C: 24-node Gauss-Legendre nodes / weights on [0,1] (fp64).
+__constant__ double c_glC_x[kGlC];
+__constant__ double c_glC_w[kGlC];
+
+struct PixelResult {
+  float g;
+  float kappa;
+  float t2n;
+  unsigned code;
+};
+
+// ---------------------------------------------------------------------------
+// a7: Legendre-Gauss integrals J_k = int_0^1 P~_k(t) exp(-lambda (t-t0)^2) dt,
+// k = 0..N+1, up to one common positive factor per pixel (the ratio eq.(29) and
+// the guard are invariant to it).  P~_k(t) = P_k(2t-1).
+//
+// Regime A (lambda >= 2, t0 in [-1,2]): the integration-by-parts idea of
+// P:411-426 applied in the Legendre basis.  With s = 2t-1, kappa = lambda/4,
+// s0 = 2t0-1, g(s) = exp(-kappa (s-s0)^2), a_k = int_{-1}^{1} P_k g ds = 2 J_k:
+//   a_{k+1} = [(2k+1)(s0 a_k - (g(1) - (-1)^k g(-1) - D_k)/(2 kappa)) - k a_{k-1}]/(k+1)
+//   D_k     = sum_{j<k, j = k-1 mod 2} (2j+1) a_j
+// (from int P_k g' = [P_k g] - int P_k' g, s P_k = ((k+1)P_{k+1} + k P_{k-1})/(2k+1)
+// and P_k' = sum (2j+1) P_j).  Seeds a_0 by two erf (eq.(31), erfcx-
+// scaled when t0 is outside [0,1]) and g(+-1) by two exp (as eq.(32)).
+// fp64 throughout: the recurrence amplifies seed errors ("Kernels").
+template <int N>
+__device__ __forceinline__ void integrals_regime_a(double lam, double t0, float J[N + 2]) {
+  const double kap = 0.25 * lam;
+  const double sk = sqrt(kap);
+  const double s0 = 2.0 * t0 - 1.0;
+  const double c = 0.88622692545275801365 / sk;  // sqrt(pi)/2 / sqrt(kappa)
+  double a0, gp, gm;
+  if (s0 < -1.0) {
+    const double x1 = sk * (-1.0 - s0), x2 = sk * (1.0 - s0);
+    const double e = exp((x1 - x2) * (x1 + x2));
+    a0 = c * (erfcx(x1) - erfcx(x2) * e);
+    gp = e;
+    gm = 1.0;
+  } else if (s0 > 1.0) {
+    const double x1 = sk * (s0 - 1.0), x2 = sk * (s0 + 1.0);
+    const double e = exp((x1 - x2) * (x1 + x2));
+    a0 = c * (erfcx(x1) - erfcx(x2) * e);
+    gp = 1.0;
+    gm = e;
+  } else {
+    const double up = 1.0 - s0, um = 1.0 + s0;
+    a0 = c * (erf(sk * up) + erf(sk * um));
+    gp = exp(-kap * up * up);
+    gm = exp(-kap * um * um);
+  }
+  const double inv2k = 2.0 / lam;  // 1/(2 kappa)
+  const double bnd_even = (gp - gm) * inv2k, bnd_odd = (gp + gm) * inv2k;
+  double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
+  J[0] = (float)a0;
+#pragma unroll
+  for (int k = 0; k <= N; ++k) {
+    const double dk = (k & 1) ? d_even : d_odd;
+    const double bk = (k & 1) ? bnd_odd : bnd_even;
+    const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
+    const double a_next = fma((double)(2 * k + 1) / (double)(k + 1), x,
+                              -((double)k / (double)(k + 1)) * a_prev);
+    if (k & 1)
+      d_odd = fma((double)(2 * k + 1), a_cur, d_odd);
+    else
+      d_even = fma((double)(2 * k + 1), a_cur, d_even);
+    a_prev = a_cur;
+    a_cur = a_next;
+    J[k + 1] = (float)a_next;
+  }
+}
+
+// Regime B (lambda < 2, t0 in [-1,2]): the integrand is smooth on [0,1]; a
+// 16-node Gauss-Legendre rule with a constant (N+2) x 16 table, fp32.
+template <int N>
+__device__ __forceinline__ void integrals_regime_b(float lam, float t0, float J[N + 2]) {
+  float E[kGlB];
+#pragma unroll
+  for (int q = 0; q < kGlB; ++q) {
+    const float z = c_glB_x[q] - t0;
+    E[q] = __expf(-lam * z * z);
+  }
+#pragma unroll
+  for (int k = 0; k <= N + 1; ++k) {
+    float s = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kGlB; ++q) s = fmaf(c_glB_W[k][q], E[q], s);
+    J[k] = s;
+  }
+}
+
+// Regime C (t0 outside [-1,2]): 24-node Gauss-Legendre on the effective
+// support [a,b] of the integrand (truncated where it has decayed by e^-24 from
+// its value at the nearer end of [0,1]), fp64, scaled by exp(lambda d^2).
+template <int N>
+__device__ __noinline__ void integrals_regime_c(double lam, double t0, float J[N + 2]) {
+  double a, b, d;
+  if (t0 < 0.0) {
+    d = -t0;
+    a = 0.0;
+    b = fmin(1.0, -d + sqrt(d * d + 24.0 / lam));
+  } else {
+    d = t0 - 1.0;
+    b = 1.0;
+    a = fmax(0.0, 1.0 - (-d + sqrt(d * d + 24.0 / lam)));
+  }
+  const double len = b - a;
+  double acc[N + 2];
+#pragma unroll
+  for (int k = 0; k <= N + 1; ++k) acc[k] = 0.0;
+  for (int q = 0; q < kGlC; ++q) {
+    const double x = fma(len, c_glC_x[q], a);
+    const double z = x - t0;
+    const double e = c_glC_w[q] * len * exp(-lam * (z - d) * (z + d));
+    const double s = 2.0 * x - 1.0;
+    double p0 = 1.0, p1 = s;
+    acc[0] += e;
+    if (N + 1 >= 1) acc[1] += e * s;
+#pragma unroll
+    for (int k = 1; k <= N; ++k) {
+      const double p2 = ((double)(2 * k + 1) * s * p1 - (double)k * p0) / (double)(k + 1);
+      acc[k + 1] += e * p2;
+      p0 = p1;
+      p1 = p2;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k <= N + 1; ++k) J[k] = (float)acc[k];
+}
+
+// ---------------------------------------------------------------------------
+// a6 + a7 + a8: from the Legendre moments nu_k = sum_j P_k(w_j) of the window
+// (w = stretched intensity in [-1,1], eq.(20)-(22)) to g-hat.
+//   T2 = sum_k (2k+1) nu_k J_k  (= sum_k c_k I_k of eq.(29), Legendre form of c = A^{-1} mu)
+//   T1/T2 = 1/2 + 1/2 sum_k nu_k [(k+1) J_{k+1} + k J_{k-1}] / T2
+//   g-hat = alpha + (beta-alpha) T1/T2                     eq.(29)
+// Guard (reading R7): T2 <= 0 or kappa > 1e3 -> the N = 0 value
+// alpha + (beta-alpha) I_1/I_0.
+template <int N>
+__device__ __forceinline__ PixelResult ghat_from_nu(const float nu[N + 1], float alpha, float beta,
+                                                    float theta, float sigma, float n,
+                                                    unsigned flags) {
+  PixelResult res;
+  res.code = 0u;
+  const double da = (double)alpha, db = (double)beta;
+  const double dd = db - da;
+  const double t0 = ((double)theta - da) / dd;            // theta_0(i)
+  const double lam = dd * dd / (2.0 * (double)sigma * (double)sigma);  // eq.(25)
+  float J[N + 2];
+  double scale_log = 0.0;  // log of the common factor applied to J (for diagnostics)
+  if (t0 < -1.0 || t0 > 2.0) {
+    integrals_regime_c<N>(lam, t0, J);
+    res.code |= kCodeFarTheta;
+    const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
+    scale_log = lam * dist * dist;
+  } else if (lam < kLambdaSmall) {
+    integrals_regime_b<N>((float)lam, (float)t0, J);
+    res.code |= kCodeSmallLambda;
+  } else {
+    integrals_regime_a<N>(lam, t0, J);
+    const double dist = t0 < 0.0 ? -t0 : (t0 > 1.0 ? t0 - 1.0 : 0.0);
+    scale_log = lam * dist * dist;
+    // regime A's J are 2x the integrals (a_k = 2 J_k)
+    scale_log += 0.69314718055994530942;
+  }
+  float T2 = 0.0f, U = 0.0f, ab = 0.0f;
+#pragma unroll
+  for (int k = 0; k <= N; ++k) {
+    const float t = (float)(2 * k + 1) * nu[k] * J[k];
+    T2 += t;
+    ab += fabsf(t);
+    const float jm = (k > 0) ? (float)k * J[k - 1] : 0.0f;
+    U = fmaf(nu[k], fmaf((float)(k + 1), J[k + 1], jm), U);
+  }
+  float ratio;
+  if (!(flags & kFlagLiteral) && (!(T2 > 0.0f) || ab > kKappaMax * T2)) {
+    ratio = J[1] / J[0];
+    res.code |= kCodeGuard;
+  } else {
+    ratio = U / T2;
+  }
+  res.kappa = (T2 > 0.0f) ? ab / T2 : CUDART_INF_F;
+  res.t2n = (float)((double)T2 / (double)n * exp(-scale_log));
+  const double mid = 0.5 * (da + db), half = 0.5 * dd;
+  float g = (float)fma(half, (double)ratio, mid);
+  if (flags & kFlagClamp) g = fminf(fmaxf(g, alpha), beta);
+  res.g = g;
+  return res;
+}
+
+// a4 + a5: from window power sums in tile units to Legendre moments.
+//   S[q] = sum_j u_j^q, q = 0..N (S[0] = n), u = (f - c_T) / s_T.
+//   au, bu = alpha, beta in the same units (exact: s_T is a power of two).
+// Taylor shift to the pixel midrange m, scaling by its half-range h gives the
+// moments of w = (u - m)/h in [-1,1] (eq.(24) P:341-345 up to the affine map
+// w = 2t - 1); the fixed Legendre table then gives nu_k = sum_j P_k(w_j).
+// Returns false (flag) when the fp64 centring amplification
+// ((1 + |m|)/h)^N exceeds 2^flag_bits ("Numerical envelope").
+template <int N>
+__device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double bu, float nu[N + 1],
+                                             float flag_bits) {
+  const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
+  const float ratio = (float)((1.0 + fabs(m)) / h);
+  if ((float)N * __log2f(ratio) > flag_bits) return false;
+#pragma unroll
+  for (int i = 1; i <= N; ++i) {
+#pragma unroll
+    for (int k = N; k >= i; --k) S[k] = fma(-m, S[k - 1], S[k]);
+  }
+  const double ih = 1.0 / h;
+  double p = ih;
+#pragma unroll
+  for (int k = 1; k <= N; ++k) {
+    S[k] *= p;
+    p *= ih;
+  }
+#pragma unroll
+  for (int k = 0; k <= N; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int r = k & 1; r <= k; r += 2) v = fma(c_leg[k][r], S[r], v);
+    nu[k] = (float)v;
+  }
+  return true;
+}
+
+__device__ __forceinline__ int reflect_index(int i, int n) {
+  // half-sample symmetric (reading R2); one fold: -n <= i < 2n
+  return i < 0 ? -i - 1 : (i >= n ? 2 * n - 1 - i : i);
+}
+
+}  // namespace fabf

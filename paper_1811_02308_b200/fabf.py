@@ -1,0 +1,204 @@
+"""ctypes binding of include/fabf.h (argument marshalling only).
+
+Names follow the C ABI: ``Plan`` wraps ``fabf_plan``/``fabf_destroy``;
+``filter``, ``filter_diag``, ``bounds`` and ``filter_host`` wrap the entry points
+of the same names.  Tensors are float32, contiguous; device tensors are passed
+by ``data_ptr()`` with ``torch.cuda.current_stream()`` unless a stream is given.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_PKG, "libfabf.so")
+
+FLAG_LITERAL = 0x1
+FLAG_CLAMP = 0x2
+CODE_IDENTITY = 0x1
+CODE_GUARD = 0x2
+CODE_SMALL_LAMBDA = 0x4
+CODE_FALLBACK = 0x8
+CODE_FAR_THETA = 0x10
+MAX_N = 10
+
+_STATUS = {0: "FABF_OK", 1: "FABF_ERR_INVALID_ARGUMENT", 2: "FABF_ERR_UNSUPPORTED",
+           3: "FABF_ERR_CUDA", 4: "FABF_ERR_OUT_OF_MEMORY"}
+
+
+class FabfError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+class _Diag(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_void_p), ("beta", ctypes.c_void_p), ("kappa", ctypes.c_void_p),
+                ("t2n", ctypes.c_void_p), ("code", ctypes.c_void_p)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load libfabf.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(library_path):
+                raise FabfError(2, f"{library_path} not built; run python -m paper_1811_02308_b200.build")
+            L = ctypes.CDLL(library_path)
+            P, i, u = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint
+            L.fabf_plan.argtypes = [ctypes.POINTER(P), i, i, i, u]
+            L.fabf_filter.argtypes = [P, P, P, P, i, i, P, P]
+            L.fabf_filter_diag.argtypes = [P, P, P, P, i, i, P, ctypes.POINTER(_Diag), P]
+            L.fabf_bounds.argtypes = [P, P, i, P, P, P]
+            L.fabf_filter_host.argtypes = [P, P, P, P, i, i, P, P]
+            L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
+            L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
+            L.fabf_destroy.argtypes = [P]
+            for fn in ("fabf_plan", "fabf_filter", "fabf_filter_diag", "fabf_bounds",
+                       "fabf_filter_host", "fabf_last_fallback_count", "fabf_destroy",
+                       "fabf_filter_profile"):
+                getattr(L, fn).restype = ctypes.c_int
+            L.fabf_status_string.argtypes = [i]
+            L.fabf_status_string.restype = ctypes.c_char_p
+            L.fabf_last_error_message.argtypes = []
+            L.fabf_last_error_message.restype = ctypes.c_char_p
+            L.fabf_version.argtypes = []
+            L.fabf_version.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def version() -> int:
+    return lib().fabf_version()
+
+
+def _check(status: int):
+    if status != 0:
+        raise FabfError(status, lib().fabf_last_error_message().decode())
+
+
+def _dev_ptr(t, name):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise FabfError(1, f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise FabfError(1, f"{name} must be contiguous float32")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Plan:
+    """fabf_plan / fabf_destroy for batch x height x width images."""
+
+    def __init__(self, batch: int, height: int, width: int, flags: int = 0):
+        self.shape = (int(batch), int(height), int(width))
+        self.flags = int(flags)
+        h = ctypes.c_void_p()
+        _check(lib().fabf_plan(ctypes.byref(h), self.shape[0], self.shape[1], self.shape[2], self.flags))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().fabf_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def last_fallback_count(self) -> int:
+        c = ctypes.c_longlong(0)
+        _check(lib().fabf_last_fallback_count(self._h, ctypes.byref(c)))
+        return int(c.value)
+
+
+def filter(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=None):
+    """fabf_filter on device tensors; returns ``out``."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(img)
+    _check(lib().fabf_filter(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
+                             _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+                             _stream_ptr(stream)))
+    return out
+
+
+def filter_diag(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=None):
+    """fabf_filter_diag: returns (out, dict(alpha, beta, kappa, t2n, code))."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(img)
+    d = {k: torch.empty_like(img) for k in ("alpha", "beta", "kappa", "t2n")}
+    d["code"] = torch.empty(img.shape, dtype=torch.uint8, device=img.device)
+    diag = _Diag(*(ctypes.c_void_p(d[k].data_ptr()) for k in ("alpha", "beta", "kappa", "t2n", "code")))
+    _check(lib().fabf_filter_diag(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
+                                  _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+                                  ctypes.byref(diag), _stream_ptr(stream)))
+    return out, d
+
+
+def bounds(plan: Plan, img, rho: int, alpha=None, beta=None, stream=None):
+    """fabf_bounds: (alpha, beta) = window (min, max)."""
+    import torch
+
+    alpha = torch.empty_like(img) if alpha is None else alpha
+    beta = torch.empty_like(img) if beta is None else beta
+    _check(lib().fabf_bounds(plan.handle, _dev_ptr(img, "img"), int(rho), _dev_ptr(alpha, "alpha"),
+                             _dev_ptr(beta, "beta"), _stream_ptr(stream)))
+    return alpha, beta
+
+
+def filter_host(plan: Plan, img, theta, sigma, rho: int, N: int, out, stream=None):
+    """fabf_filter_host on HOST buffers (numpy arrays or CPU tensors, ideally
+    pinned); copies in, filters, copies out, synchronises."""
+    def hp(a, name):
+        if hasattr(a, "data_ptr"):
+            if a.is_cuda or not a.is_contiguous():
+                raise FabfError(1, f"{name} must be a contiguous host tensor")
+            return ctypes.c_void_p(a.data_ptr())
+        if not a.flags["C_CONTIGUOUS"] or a.dtype.itemsize != 4:
+            raise FabfError(1, f"{name} must be contiguous float32")
+        return ctypes.c_void_p(a.ctypes.data)
+
+    _check(lib().fabf_filter_host(plan.handle, hp(img, "img"), hp(theta, "theta"), hp(sigma, "sigma"),
+                                  int(rho), int(N), hp(out, "out"), _stream_ptr(stream)))
+    return out
+
+
+def filter_profile(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=None):
+    """fabf_filter_profile: returns (out, [ms bounds-rows, bounds-cols, filter, fallback])."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(img)
+    ms = (ctypes.c_float * 4)()
+    _check(lib().fabf_filter_profile(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
+                                     _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+                                     _stream_ptr(stream), ms))
+    return out, [float(v) for v in ms]
