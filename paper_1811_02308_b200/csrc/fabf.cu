@@ -50,6 +50,7 @@ constexpr int kBoundsTX = 256;  // outputs per CTA row task (rows pass)
 constexpr int kBoundsCX = 32;   // columns per CTA (columns pass)
 constexpr int kMaxRho = 96;     // L = TW + 2 rho <= 256 input columns per strip
 constexpr float kFlagBits = 26.0f;
+constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // opt-in limit minus static shared memory
 
 using Plan = fabf_plan_s;
 
@@ -593,11 +594,11 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     FABF_CUDA(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024),
+                                   kMaxDynSmem),
               "cudaFuncSetAttribute(k_filter)");
     attr_set = true;
   }
-  if (smem > 227 * 1024) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
+  if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
   dim3 grid((fa.W + fa.TW - 1) / fa.TW, (fa.H + fa.SH - 1) / fa.SH, B);
   k_filter<N><<<grid, kThreads, smem, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
