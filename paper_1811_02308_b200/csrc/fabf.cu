@@ -46,8 +46,6 @@ struct fabf_plan_s {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBoundsTX = 256;  // outputs per CTA row task (rows pass)
-constexpr int kBoundsCX = 32;   // columns per CTA (columns pass)
 constexpr int kMaxRho = 96;     // L = TW + 2 rho <= 256 input columns per strip
 constexpr float kFlagBits = 26.0f;
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // opt-in limit minus static shared memory
@@ -111,17 +109,6 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
 fabf_status_t ensure_tables(int dev) {
   std::lock_guard<std::mutex> lk(g_tables_mu);
   if (dev >= 0 && dev < 64 && g_tables_ready[dev]) return FABF_OK;
-  // Legendre coefficients, (k+1) P_{k+1} = (2k+1) w P_k - k P_{k-1}
-  double leg[kMaxN + 1][kMaxN + 1] = {};
-  leg[0][0] = 1.0;
-  leg[1][1] = 1.0;
-  for (int k = 1; k < kMaxN; ++k)
-    for (int r = 0; r <= k + 1; ++r) {
-      double v = 0.0;
-      if (r >= 1) v += (2 * k + 1) * leg[k][r - 1];
-      v -= k * leg[k - 1][r];
-      leg[k + 1][r] = v / (k + 1);
-    }
   std::vector<double> xb, wb, xc, wc;
   gauss_legendre(kGlB, xb, wb);
   gauss_legendre(kGlC, xc, wc);
@@ -138,7 +125,6 @@ fabf_status_t ensure_tables(int dev) {
       p1 = p2;
     }
   }
-  FABF_CUDA(cudaMemcpyToSymbol(c_leg, leg, sizeof(leg)), "cudaMemcpyToSymbol(c_leg)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glB_x, bx, sizeof(bx)), "cudaMemcpyToSymbol(c_glB_x)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glB_W, bW, sizeof(bW)), "cudaMemcpyToSymbol(c_glB_W)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glC_x, xc.data(), sizeof(double) * kGlC), "cudaMemcpyToSymbol(c_glC_x)");
@@ -150,138 +136,120 @@ fabf_status_t ensure_tables(int dev) {
 }  // namespace
 
 // ============================================================================
-// step a1: bounds.  Rows pass: grid (ceil(W/TX), H, B).  Each CTA stages the
-// row segment [x0-rho, x0+TX+rho) (reflected) and computes, per block of
-// w = 2rho+1 staged samples, the prefix and suffix min/max (one thread per
-// block and direction); output x takes min(S[x], P[x+2rho]) (van Herk /
-// Gil-Werman: 3 comparisons per sample and pass, independent of rho).
+// step a1: bounds (eq.(8)) -- separable sliding min/max, one pass per
+// direction, each by log-doubling in shared memory: M_1 = f,
+// M_2j(x) = op(M_j(x), M_j(x+j)); the window [x, x+w-1] is
+// op(M_K(x), M_K(x+w-K)) with K the largest power of two <= w.  ceil(log2 w)
+// comparisons per sample and pass, independent of the image content; min and
+// max travel together as float2.  Comparisons only: bit-exact.
+constexpr int kRowsTX = 256;  // outputs per CTA row (rows pass)
+constexpr int kRowsRY = 4;    // rows per CTA (rows pass)
+constexpr int kColsCX = 32;   // columns per CTA (columns pass)
+
+__device__ __forceinline__ float2 mm2(float2 a, float2 b) {
+  return make_float2(fminf(a.x, b.x), fmaxf(a.y, b.y));
+}
+
 __global__ void __launch_bounds__(kThreads) k_bounds_rows(const float* __restrict__ img, int H,
                                                            int W, int rho,
                                                            float* __restrict__ hmin,
                                                            float* __restrict__ hmax) {
-  extern __shared__ float sm[];
+  extern __shared__ float2 sm2[];
   const int w = 2 * rho + 1;
-  const int x0 = blockIdx.x * kBoundsTX;
-  const int y = blockIdx.y;
+  const int LS = kRowsTX + 2 * kMaxRho;  // row stride of the staging buffers
+  const int x0 = blockIdx.x * kRowsTX;
+  const int y0 = blockIdx.y * kRowsRY;
   const size_t plane = (size_t)blockIdx.z * H * W;
-  const int nout = min(kBoundsTX, W - x0);
+  const int nout = min(kRowsTX, W - x0);
+  const int nrow = min(kRowsRY, H - y0);
   const int L = nout + 2 * rho;
-  float* f = sm;
-  float* Pmin = f + (kBoundsTX + 2 * kMaxRho);
-  float* Pmax = Pmin + (kBoundsTX + 2 * kMaxRho);
-  float* Smin = Pmax + (kBoundsTX + 2 * kMaxRho);
-  float* Smax = Smin + (kBoundsTX + 2 * kMaxRho);
-  const float* row = img + plane + (size_t)y * W;
-  for (int c = threadIdx.x; c < L; c += blockDim.x) f[c] = row[reflect_index(x0 - rho + c, W)];
-  __syncthreads();
-  const int nb = (L + w - 1) / w;
-  for (int t = threadIdx.x; t < 2 * nb; t += blockDim.x) {
-    const int blk = t >> 1;
-    const int s = blk * w, e = min(L, s + w);
-    if ((t & 1) == 0) {
-      float mn = f[s], mx = f[s];
-      Pmin[s] = mn;
-      Pmax[s] = mx;
-      for (int c = s + 1; c < e; ++c) {
-        const float v = f[c];
-        mn = fminf(mn, v);
-        mx = fmaxf(mx, v);
-        Pmin[c] = mn;
-        Pmax[c] = mx;
-      }
-    } else {
-      float mn = f[e - 1], mx = f[e - 1];
-      Smin[e - 1] = mn;
-      Smax[e - 1] = mx;
-      for (int c = e - 2; c >= s; --c) {
-        const float v = f[c];
-        mn = fminf(mn, v);
-        mx = fmaxf(mx, v);
-        Smin[c] = mn;
-        Smax[c] = mx;
-      }
-    }
+  float2* bufA = sm2;
+  float2* bufB = sm2 + kRowsRY * LS;
+  for (int i = threadIdx.x; i < nrow * L; i += blockDim.x) {
+    const int r = i / L, c = i - r * L;
+    const float v = __ldg(img + plane + (size_t)(y0 + r) * W + reflect_index(x0 - rho + c, W));
+    bufA[r * LS + c] = make_float2(v, v);
   }
   __syncthreads();
-  float* omin = hmin + plane + (size_t)y * W + x0;
-  float* omax = hmax + plane + (size_t)y * W + x0;
-  for (int x = threadIdx.x; x < nout; x += blockDim.x) {
-    omin[x] = fminf(Smin[x], Pmin[x + 2 * rho]);
-    omax[x] = fmaxf(Smax[x], Pmax[x + 2 * rho]);
+  int K = 1;
+  while (2 * K <= w) {
+    const int lim = L - 2 * K + 1;  // M_2K valid for x < lim
+    for (int i = threadIdx.x; i < nrow * lim; i += blockDim.x) {
+      const int r = i / lim, c = i - r * lim;
+      bufB[r * LS + c] = mm2(bufA[r * LS + c], bufA[r * LS + c + K]);
+    }
+    __syncthreads();
+    float2* t = bufA;
+    bufA = bufB;
+    bufB = t;
+    K *= 2;
+  }
+  for (int i = threadIdx.x; i < nrow * nout; i += blockDim.x) {
+    const int r = i / nout, x = i - r * nout;
+    const float2 v = mm2(bufA[r * LS + x], bufA[r * LS + x + w - K]);
+    const size_t o = plane + (size_t)(y0 + r) * W + x0 + x;
+    hmin[o] = v.x;
+    hmax[o] = v.y;
   }
 }
 
-// Columns pass: grid (ceil(W/32), ceil(H/TY), B), block (32, 8).  Same van
-// Herk / Gil-Werman scheme along y on the row-pass output.
+// Columns pass: block (32, 8), a band of 32 columns x TY output rows.
 __global__ void __launch_bounds__(kThreads) k_bounds_cols(const float* __restrict__ hmin,
                                                            const float* __restrict__ hmax, int H,
                                                            int W, int rho, int TY,
                                                            float* __restrict__ amin,
                                                            float* __restrict__ bmax) {
-  extern __shared__ float sm[];
+  extern __shared__ float2 sm2[];
   const int w = 2 * rho + 1;
-  const int x0 = blockIdx.x * kBoundsCX;
+  const int x0 = blockIdx.x * kColsCX;
   const int y0 = blockIdx.y * TY;
   const size_t plane = (size_t)blockIdx.z * H * W;
   const int nrow = min(TY, H - y0);
   const int L = nrow + 2 * rho;
   const int LS = TY + 2 * rho;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  float* vmin = sm;
-  float* vmax = vmin + LS * kBoundsCX;
-  float* Pmin = vmax + LS * kBoundsCX;
-  float* Pmax = Pmin + LS * kBoundsCX;
-  float* Smin = Pmax + LS * kBoundsCX;
-  float* Smax = Smin + LS * kBoundsCX;
   const int x = x0 + tx;
   const bool colok = x < W;
+  float2* bufA = sm2;
+  float2* bufB = sm2 + LS * kColsCX;
   for (int r = ty; r < L; r += blockDim.y) {
-    const int yy = reflect_index(y0 - rho + r, H);
-    const size_t o = plane + (size_t)yy * W + (colok ? x : 0);
-    vmin[r * kBoundsCX + tx] = colok ? hmin[o] : 0.0f;
-    vmax[r * kBoundsCX + tx] = colok ? hmax[o] : 0.0f;
+    const size_t o = plane + (size_t)reflect_index(y0 - rho + r, H) * W + (colok ? x : 0);
+    bufA[r * kColsCX + tx] = make_float2(__ldg(hmin + o), __ldg(hmax + o));
   }
   __syncthreads();
-  const int nb = (L + w - 1) / w;
-  // task = (block, direction), tx = column
-  for (int t = ty; t < 2 * nb; t += blockDim.y) {
-    const int blk = t >> 1;
-    const int s = blk * w, e = min(L, s + w);
-    if ((t & 1) == 0) {
-      float mn = vmin[s * kBoundsCX + tx], mx = vmax[s * kBoundsCX + tx];
-      Pmin[s * kBoundsCX + tx] = mn;
-      Pmax[s * kBoundsCX + tx] = mx;
-      for (int r = s + 1; r < e; ++r) {
-        mn = fminf(mn, vmin[r * kBoundsCX + tx]);
-        mx = fmaxf(mx, vmax[r * kBoundsCX + tx]);
-        Pmin[r * kBoundsCX + tx] = mn;
-        Pmax[r * kBoundsCX + tx] = mx;
-      }
-    } else {
-      float mn = vmin[(e - 1) * kBoundsCX + tx], mx = vmax[(e - 1) * kBoundsCX + tx];
-      Smin[(e - 1) * kBoundsCX + tx] = mn;
-      Smax[(e - 1) * kBoundsCX + tx] = mx;
-      for (int r = e - 2; r >= s; --r) {
-        mn = fminf(mn, vmin[r * kBoundsCX + tx]);
-        mx = fmaxf(mx, vmax[r * kBoundsCX + tx]);
-        Smin[r * kBoundsCX + tx] = mn;
-        Smax[r * kBoundsCX + tx] = mx;
-      }
-    }
+  int K = 1;
+  while (2 * K <= w) {
+    const int lim = L - 2 * K + 1;
+    for (int r = ty; r < lim; r += blockDim.y)
+      bufB[r * kColsCX + tx] = mm2(bufA[r * kColsCX + tx], bufA[(r + K) * kColsCX + tx]);
+    __syncthreads();
+    float2* t = bufA;
+    bufA = bufB;
+    bufB = t;
+    K *= 2;
   }
-  __syncthreads();
   if (!colok) return;
   for (int r = ty; r < nrow; r += blockDim.y) {
+    const float2 v = mm2(bufA[r * kColsCX + tx], bufA[(r + w - K) * kColsCX + tx]);
     const size_t o = plane + (size_t)(y0 + r) * W + x;
-    amin[o] = fminf(Smin[r * kBoundsCX + tx], Pmin[(r + 2 * rho) * kBoundsCX + tx]);
-    bmax[o] = fmaxf(Smax[r * kBoundsCX + tx], Pmax[(r + 2 * rho) * kBoundsCX + tx]);
+    amin[o] = v.x;
+    bmax[o] = v.y;
   }
 }
 
 // ============================================================================
-// steps a3-a8.  Grid (ceil(W/TW), ceil(H/SH), B), 256 threads, RB = 256/TW
-// output rows per step.  Shared memory: f ring [w][L] (fp32) and the per-step
-// prefix-sum buffer [RB][N][L] (fp64).  L = TW + 2 rho <= 256.
+// steps a2-a8.  Grid (ceil(W/TW), ceil(H/SH), B), 256 threads, RB = 256/TW
+// output rows per step.  Per step:
+//   A  column owners (thread c < L = TW + 2rho) add the entering row's powers
+//      to / remove the leaving row's powers from their fp64 vertical sums V_q
+//      (kept in shared memory between steps) and write them to Ps;
+//   B  one warp per (row, q): inclusive prefix scan of Ps along the strip
+//      (lane-transposed layout pos(c) = (c % E)*32 + c / E: conflict-free);
+//   C1 one pixel per thread: window sums = prefix differences, stretch to
+//      Legendre moments (fp64), range parameters, regime; the record goes to a
+//      shared-memory queue, regime-A records from the front, B/C from the back;
+//   C2 thread j finishes queue record j (integrals, ratio, guard, store), so
+//      warps run one integral regime each except at the A|B boundary.
 struct FilterArgs {
   const float* img;
   const float* theta;
@@ -300,8 +268,40 @@ struct FilterArgs {
 };
 
 template <int N>
+struct FilterSmem {
+  // byte offsets into dynamic shared memory
+  size_t ps, vs, qnu, qlam, qt0, qal, qbe, qo, qreg, total;
+  __host__ __device__ FilterSmem(int L, int E, int w, int RB) {
+    const int NN = N > 0 ? N : 1;
+    size_t off = 0;
+    ps = off;
+    off += sizeof(double) * (size_t)RB * NN * 32 * E;
+    vs = off;
+    off += sizeof(double) * (size_t)NN * L;
+    qnu = off;
+    off += sizeof(float) * (size_t)(N + 1) * kThreads;
+    qlam = off;
+    off += sizeof(float) * kThreads;
+    qt0 = off;
+    off += sizeof(float) * kThreads;
+    qal = off;
+    off += sizeof(float) * kThreads;
+    qbe = off;
+    off += sizeof(float) * kThreads;
+    qo = off;
+    off += sizeof(int) * kThreads;
+    qreg = off;
+    off += sizeof(int) * kThreads;
+    total = off;
+  }
+};
+
+template <int N>
 __global__ void __launch_bounds__(kThreads, 2) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int cntA, cntBC;
+  __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
+  constexpr int NN = N > 0 ? N : 1;
   const int rho = a.rho, w = 2 * rho + 1, TW = a.TW;
   const int RB = kThreads / TW;
   const int x0 = blockIdx.x * TW;
@@ -309,31 +309,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter(FilterArgs a) {
   const int H = a.H, W = a.W;
   const int Y1 = min(H, Y0 + a.SH);  // output rows [Y0, Y1)
   const int L = TW + 2 * rho;
+  const int E = (L + 31) >> 5;
   const size_t plane = (size_t)blockIdx.z * H * W;
-  const int tid = threadIdx.x;
-  double* Ps = reinterpret_cast<double*>(smraw);            // [RB][N][L]
-  float* fring = reinterpret_cast<float*>(Ps + (size_t)RB * (N > 0 ? N : 1) * L);  // [w][L]
-  __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const FilterSmem<N> lay(L, E, w, RB);
+  double* Ps = reinterpret_cast<double*>(smraw + lay.ps);  // [RB][N][32*E]
+  double* Vs = reinterpret_cast<double*>(smraw + lay.vs);  // [N][L]
+  float* qnu = reinterpret_cast<float*>(smraw + lay.qnu);   // [N+1][256]
+  float* qlam = reinterpret_cast<float*>(smraw + lay.qlam);
+  float* qt0 = reinterpret_cast<float*>(smraw + lay.qt0);
+  float* qal = reinterpret_cast<float*>(smraw + lay.qal);
+  float* qbe = reinterpret_cast<float*>(smraw + lay.qbe);
+  int* qo = reinterpret_cast<int*>(smraw + lay.qo);
+  int* qreg = reinterpret_cast<int*>(smraw + lay.qreg);
+  const int PSQ = 32 * E;  // one (row, q) prefix row
 
   // ---- tile-local centre c_T and power-of-two scale s_T from the bounds of
   // ---- the tile's outputs (their windows cover exactly the tile footprint)
   float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
   {
     const int ox = x0 + (tid % TW);
-    for (int yy = Y0 + tid / TW; yy < Y1; yy += RB) {
-      if (ox < W) {
+    if (ox < W) {
+      for (int yy = Y0 + tid / TW; yy < Y1; yy += RB) {
         const size_t o = plane + (size_t)yy * W + ox;
-        lmin = fminf(lmin, a.alpha[o]);
-        lmax = fmaxf(lmax, a.beta[o]);
+        lmin = fminf(lmin, __ldg(a.alpha + o));
+        lmax = fmaxf(lmax, __ldg(a.beta + o));
       }
     }
     for (int off = 16; off > 0; off >>= 1) {
       lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
       lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
     }
-    if ((tid & 31) == 0) {
-      red_min[tid >> 5] = lmin;
-      red_max[tid >> 5] = lmax;
+    if (lane == 0) {
+      red_min[warp] = lmin;
+      red_max[warp] = lmax;
     }
     __syncthreads();
     lmin = red_min[0];
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter(FilterArgs a) {
     }
   }
   const double cT = 0.5 * ((double)lmin + (double)lmax);
-  double halfr = 0.5 * ((double)lmax - (double)lmin);
+  const double halfr = 0.5 * ((double)lmax - (double)lmin);
   int e2 = 0;
   if (halfr > 0.0) frexp(halfr, &e2);
   const double invS = ldexp(1.0, -e2);  // 1/s_T, s_T = 2^e2 >= half range: exact scaling
@@ -353,70 +362,87 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter(FilterArgs a) {
   const int c = tid;
   const bool owner = c < L;
   const int xin = reflect_index(min(x0 - rho + c, W - 1 + rho), W);
-  double V[N + 1];
-#pragma unroll
-  for (int q = 0; q <= N; ++q) V[q] = 0.0;
-  const int ystart = Y0 - rho;
-  int slot = 0, loaded = 0;
+  const int pos_c = (c % E) * 32 + c / E;
+  const float* colp = a.img + plane + xin;  // this thread's input column
 
-  auto enter_row = [&](int yin) {
-    // one entering row for this column: ring update + running power sums
-    if (!owner) return;
-    const float fv = a.img[plane + (size_t)reflect_index(yin, H) * W + xin];
-    float* cell = fring + (size_t)slot * L + c;
-    const float fo = *cell;
-    *cell = fv;
-    const double u = ((double)fv - cT) * invS;
-    if (loaded >= w) {
-      const double uo = ((double)fo - cT) * invS;
-      double pu = u, po = uo;
+  // prologue: rows Y0-rho .. Y0+rho-1 (no outputs yet); V starts at zero
+  if (owner) {
+    double V[NN];
 #pragma unroll
-      for (int q = 1; q <= N; ++q) {
-        V[q] += pu - po;
-        pu *= u;
-        po *= uo;
-      }
-    } else {
+    for (int q = 0; q < NN; ++q) V[q] = 0.0;
+    for (int yin = Y0 - rho; yin < Y0 + rho; ++yin) {
+      const float fv = __ldg(colp + (size_t)reflect_index(yin, H) * W);
+      const double u = ((double)fv - cT) * invS;
       double pu = u;
 #pragma unroll
-      for (int q = 1; q <= N; ++q) {
+      for (int q = 0; q < N; ++q) {
         V[q] += pu;
         pu *= u;
       }
     }
-    slot = (slot + 1 == w) ? 0 : slot + 1;
-    ++loaded;
-  };
-
-  // prologue: rows ystart .. Y0 + rho - 1 (no outputs yet)
-  for (int yin = ystart; yin < Y0 + rho; ++yin) enter_row(yin);
-  if (!owner) loaded += 2 * rho;  // keep counters consistent (unused)
+#pragma unroll
+    for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
+  }
 
   const float n = (float)(w * w);
-  const int lane = tid & 31, warp = tid >> 5;
-  const int E = (L + 31) / 32;
+  const int px_r = tid / TW, px_x = tid % TW;
+  const int pos_hi = ((px_x + 2 * rho) % E) * 32 + (px_x + 2 * rho) / E;
+  const int pos_lo = px_x > 0 ? ((px_x - 1) % E) * 32 + (px_x - 1) / E : 0;
+  const bool want_t2n = a.d_t2n != nullptr;
 
   for (int Yb = Y0; Yb < Y1; Yb += RB) {
     const int nr = min(RB, Y1 - Yb);
-    // ---- phase A: entering rows Yb+r+rho, write V into the prefix buffer
-    for (int r = 0; r < nr; ++r) {
-      enter_row(Yb + r + rho);
-      if (owner) {
+    // prefetch this thread's pixel parameters (latency hidden behind A and B)
+    const int pY = Yb + px_r, pX = x0 + px_x;
+    const bool pvalid = (px_r < nr) && (pX < W);
+    const size_t po = plane + (size_t)pY * W + pX;
+    float p_al = 0.f, p_be = 0.f, p_th = 0.f, p_sg = 1.f;
+    if (pvalid) {
+      p_al = __ldg(a.alpha + po);
+      p_be = __ldg(a.beta + po);
+      p_th = __ldg(a.theta + po);
+      p_sg = __ldg(a.sigma + po);
+    }
+    if (tid == 0) {
+      cntA = 0;
+      cntBC = 0;
+    }
+    // ---- phase A
+    if (owner) {
+      double V[NN];
 #pragma unroll
-        for (int q = 1; q <= N; ++q) Ps[((size_t)r * N + (q - 1)) * L + c] = V[q];
+      for (int q = 0; q < N; ++q) V[q] = Vs[(size_t)q * L + c];
+      for (int r = 0; r < nr; ++r) {
+        // entering row Yb+r+rho, leaving row Yb+r-rho-1 (re-read: L2-resident)
+        const int yin = Yb + r + rho, yout = yin - w;
+        const float fv = __ldg(colp + (size_t)reflect_index(yin, H) * W);
+        const bool leave = yout >= Y0 - rho;
+        const float fo = leave ? __ldg(colp + (size_t)reflect_index(yout, H) * W) : 0.0f;
+        const double u = ((double)fv - cT) * invS;
+        const double uo = leave ? ((double)fo - cT) * invS : 0.0;
+        double pu = u, po2 = uo;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          V[q] += pu - po2;
+          pu *= u;
+          po2 *= uo;
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q) Ps[((size_t)r * NN + q) * PSQ + pos_c] = V[q];
       }
+#pragma unroll
+      for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
     }
     __syncthreads();
-    // ---- phase B: inclusive prefix sums over c for each (r, q), one warp per scan
+    // ---- phase B: inclusive prefix sums over c for each (r, q)
     if (N > 0) {
       for (int s = warp; s < nr * N; s += kThreads / 32) {
-        double* row = Ps + (size_t)s * L;
+        double* row = Ps + (size_t)s * PSQ;
         double loc[8];
         double tot = 0.0;
-        const int cb = lane * E;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          if (e < E && cb + e < L) tot += row[cb + e];
+          if (e < E) tot += row[e * 32 + lane];
           loc[e] = tot;
         }
         double inc = tot;
@@ -425,51 +451,82 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter(FilterArgs a) {
           const double v = __shfl_up_sync(0xffffffffu, inc, off);
           if (lane >= off) inc += v;
         }
-        const double excl = inc - tot;
+        // exclusive offset straight from the neighbour (never inc - tot: a lane
+        // whose chunk runs into the padding carries garbage in tot)
+        double excl = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) excl = 0.0;
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          if (e < E && cb + e < L) row[cb + e] = loc[e] + excl;
+          if (e < E) row[e * 32 + lane] = loc[e] + excl;
       }
     }
     __syncthreads();
-    // ---- phase C: one output pixel per thread
+    // ---- phase C1: stretch + range parameters + enqueue
     {
-      const int r = tid / TW, x = tid % TW;
-      const int Y = Yb + r, X = x0 + x;
-      if (r < nr && X < W) {
-        const size_t o = plane + (size_t)Y * W + X;
-        const float al = a.alpha[o], be = a.beta[o];
-        PixelResult res;
-        bool done = true;
-        if (al == be) {  // P:204, Algorithm 1 lines 4-5
-          res.g = a.img[o];
-          res.kappa = 1.0f;
-          res.t2n = 1.0f;
-          res.code = kCodeIdentity;
+      int regime = -1;  // -1: no record (invalid, identity or fallback)
+      float nu[N + 1];
+      float lam = 0.f, t0 = 0.f;
+      if (pvalid) {
+        if (p_al == p_be) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
+          a.out[po] = p_al;
+          if (a.d_kappa) a.d_kappa[po] = 1.0f;
+          if (a.d_t2n) a.d_t2n[po] = 1.0f;
+          if (a.d_code) a.d_code[po] = (unsigned char)kCodeIdentity;
         } else {
           double S[N + 1];
           S[0] = (double)n;
 #pragma unroll
           for (int q = 1; q <= N; ++q) {
-            const double* row = Ps + ((size_t)r * N + (q - 1)) * L;
-            S[q] = row[x + 2 * rho] - (x > 0 ? row[x - 1] : 0.0);
+            const double* row = Ps + ((size_t)px_r * NN + (q - 1)) * PSQ;
+            S[q] = row[pos_hi] - (px_x > 0 ? row[pos_lo] : 0.0);
           }
-          float nu[N + 1];
-          const double au = ((double)al - cT) * invS, bu = ((double)be - cT) * invS;
+          const double au = ((double)p_al - cT) * invS, bu = ((double)p_be - cT) * invS;
           if (nu_from_sums<N>(S, au, bu, nu, a.flag_bits)) {
-            res = ghat_from_nu<N>(nu, al, be, a.theta[o], a.sigma[o], n, a.flags);
-          } else {
-            done = false;  // exact-moment fallback pass writes this pixel
+            regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
+          } else {  // exact-moment fallback pass writes this pixel
             const int slotfb = atomicAdd(a.fb_count, 1);
-            a.fb_list[slotfb] = (int)(o);
+            a.fb_list[slotfb] = (int)po;
           }
         }
-        if (done) {
-          a.out[o] = res.g;
-          if (a.d_kappa) a.d_kappa[o] = res.kappa;
-          if (a.d_t2n) a.d_t2n[o] = res.t2n;
-          if (a.d_code) a.d_code[o] = (unsigned char)res.code;
-        }
+      }
+      const unsigned mA = __ballot_sync(0xffffffffu, regime == kRegA);
+      const unsigned mB = __ballot_sync(0xffffffffu, regime > kRegA);
+      int baseA = 0, baseB = 0;
+      if (lane == 0) {
+        if (mA) baseA = atomicAdd(&cntA, __popc(mA));
+        if (mB) baseB = atomicAdd(&cntBC, __popc(mB));
+      }
+      baseA = __shfl_sync(0xffffffffu, baseA, 0);
+      baseB = __shfl_sync(0xffffffffu, baseB, 0);
+      const unsigned lt = (1u << lane) - 1u;
+      if (regime >= 0) {
+        const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
+                                        : kThreads - 1 - (baseB + __popc(mB & lt));
+#pragma unroll
+        for (int k = 0; k <= N; ++k) qnu[k * kThreads + j] = nu[k];
+        qlam[j] = lam;
+        qt0[j] = t0;
+        qal[j] = p_al;
+        qbe[j] = p_be;
+        qo[j] = (int)po;
+        qreg[j] = regime;
+      }
+    }
+    __syncthreads();
+    // ---- phase C2: integrals, ratio, guard, store (one regime per warp)
+    {
+      const int j = tid;
+      if (j < cntA || j >= kThreads - cntBC) {
+        float nu[N + 1];
+#pragma unroll
+        for (int k = 0; k <= N; ++k) nu[k] = qnu[k * kThreads + j];
+        const int o = qo[j];
+        PixelResult res = ghat_from_record<N>(nu, qlam[j], qt0[j], qal[j], qbe[j], qreg[j],
+                                              a.flags, want_t2n, n);
+        a.out[o] = res.g;
+        if (a.d_kappa) a.d_kappa[o] = res.kappa;
+        if (a.d_t2n) a.d_t2n[o] = res.t2n;
+        if (a.d_code) a.d_code[o] = (unsigned char)res.code;
       }
     }
     __syncthreads();
@@ -492,8 +549,8 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
     const int o = a.fb_list[i];
     const int b = o / (H * W), rem = o - b * H * W, y = rem / W, x = rem - y * W;
     const float* img = a.img + (size_t)b * H * W;
-    const double al = a.alpha[o], be = a.beta[o];
-    const double mid = 0.5 * (al + be), ih = 2.0 / (be - al);
+    const float al = a.alpha[o], be = a.beta[o];
+    const double mid = 0.5 * ((double)al + (double)be), ih = 2.0 / ((double)be - (double)al);
     double acc[N + 1];
 #pragma unroll
     for (int k = 0; k <= N; ++k) acc[k] = 0.0;
@@ -519,8 +576,10 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
       float nu[N + 1];
 #pragma unroll
       for (int k = 0; k <= N; ++k) nu[k] = (float)acc[k];
-      PixelResult res = ghat_from_nu<N>(nu, (float)al, (float)be, a.theta[o], a.sigma[o],
-                                        (float)n, a.flags);
+      float lam, t0;
+      const int regime = range_params(al, be, a.theta[o], a.sigma[o], lam, t0);
+      PixelResult res = ghat_from_record<N>(nu, lam, t0, al, be, regime, a.flags,
+                                            a.d_t2n != nullptr, (float)n);
       a.out[o] = res.g;
       if (a.d_kappa) a.d_kappa[o] = res.kappa;
       if (a.d_t2n) a.d_t2n[o] = res.t2n;
@@ -563,15 +622,14 @@ inline void prof_mark(int i, cudaStream_t st) {
 
 fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta,
                             cudaStream_t st) {
-  const size_t smem_rows = sizeof(float) * 5 * (kBoundsTX + 2 * kMaxRho);
-  dim3 g1((p->W + kBoundsTX - 1) / kBoundsTX, p->H, p->B);
+  const size_t smem_rows = sizeof(float2) * 2 * kRowsRY * (kRowsTX + 2 * kMaxRho);
+  dim3 g1((p->W + kRowsTX - 1) / kRowsTX, (p->H + kRowsRY - 1) / kRowsRY, p->B);
   prof_mark(0, st);
   k_bounds_rows<<<g1, kThreads, smem_rows, st>>>(img, p->H, p->W, rho, p->hmin, p->hmax);
   FABF_CUDA(cudaGetLastError(), "k_bounds_rows launch");
   prof_mark(1, st);
-  int TY = 64;
-  while (TY > 8 && sizeof(float) * 6 * (TY + 2 * rho) * kBoundsCX > 160 * 1024) TY >>= 1;
-  const size_t smem_cols = sizeof(float) * 6 * (TY + 2 * rho) * kBoundsCX;
+  const int TY = 64;
+  const size_t smem_cols = sizeof(float2) * 2 * (TY + 2 * rho) * kColsCX;
   static bool attr_set = false;
   if (!attr_set) {
     FABF_CUDA(cudaFuncSetAttribute(k_bounds_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -579,8 +637,8 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
               "cudaFuncSetAttribute(k_bounds_cols)");
     attr_set = true;
   }
-  dim3 g2((p->W + kBoundsCX - 1) / kBoundsCX, (p->H + TY - 1) / TY, p->B);
-  k_bounds_cols<<<g2, dim3(kBoundsCX, kThreads / kBoundsCX), smem_cols, st>>>(
+  dim3 g2((p->W + kColsCX - 1) / kColsCX, (p->H + TY - 1) / TY, p->B);
+  k_bounds_cols<<<g2, dim3(kColsCX, kThreads / kColsCX), smem_cols, st>>>(
       p->hmin, p->hmax, p->H, p->W, rho, TY, alpha, beta);
   FABF_CUDA(cudaGetLastError(), "k_bounds_cols launch");
   prof_mark(2, st);
@@ -590,7 +648,7 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
 template <int N>
 fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   const int L = fa.TW + 2 * fa.rho, w = 2 * fa.rho + 1, RB = kThreads / fa.TW;
-  const size_t smem = sizeof(double) * RB * (N > 0 ? N : 1) * L + sizeof(float) * w * L;
+  const size_t smem = FilterSmem<N>(L, (L + 31) / 32, w, RB).total;
   static bool attr_set = false;
   if (!attr_set) {
     FABF_CUDA(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -27,8 +27,6 @@ constexpr unsigned kCodeFarTheta = 0x10u;
 constexpr unsigned kFlagLiteral = 0x1u;
 constexpr unsigned kFlagClamp = 0x2u;
 
-// Legendre polynomial coefficients on [-1,1]: P_k(w) = sum_r leg[k][r] w^r.
-__constant__ double c_leg[kMaxN + 1][kMaxN + 1];
 // Regime B: W[k][q] = w_q * P~_k(x_q), 16-node Gauss-Legendre on [0,1].
 __constant__ float c_glB_x[kGlB];
 __constant__ float c_glB_W[kMaxN + 2][kGlB];
@@ -54,35 +52,33 @@ struct PixelResult {
 //   a_{k+1} = [(2k+1)(s0 a_k - (g(1) - (-1)^k g(-1) - D_k)/(2 kappa)) - k a_{k-1}]/(k+1)
 //   D_k     = sum_{j<k, j = k-1 mod 2} (2j+1) a_j
 // (from int P_k g' = [P_k g] - int P_k' g, s P_k = ((k+1)P_{k+1} + k P_{k-1})/(2k+1)
-// and P_k' = sum (2j+1) P_j).  Seeds a_0 by two erf (eq.(31), erfcx-
-// scaled when t0 is outside [0,1]) and g(+-1) by two exp (as eq.(32)).
-// fp64 throughout: the recurrence amplifies seed errors ("Kernels").
+// and P_k' = sum (2j+1) P_j).  Seeds: a_0 by two erf (eq.(31)) written
+// as erfc = erfcx * exp so that the two boundary exponentials g(+-1) (as in
+// eq.(32)) are reused -- 2 erfcx + 2 exp, branch-free; when t0 is
+// outside [0,1] everything is scaled by exp(kappa (nearer boundary distance)^2).
+// fp64 throughout: the recurrence amplifies seed error ("Kernels").
+// lam and t0 arrive rounded to fp32; kappa is re-derived from the fp32 sqrt so
+// that the seeds and the recurrence describe one and the same problem.
 template <int N>
-__device__ __forceinline__ void integrals_regime_a(double lam, double t0, float J[N + 2]) {
-  const double kap = 0.25 * lam;
-  const double sk = sqrt(kap);
-  const double s0 = 2.0 * t0 - 1.0;
+__device__ __forceinline__ void integrals_regime_a(float lam, float t0, float J[N + 2]) {
+  const double sk = (double)sqrtf(0.25f * lam);
+  const double kap = sk * sk;
+  const double s0 = 2.0 * (double)t0 - 1.0;
+  const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);  // s = +1 and s = -1 ends
+  const double qa = xa * xa, qb = xb * xb;
+  const bool a_near = qa < qb;
+  const double qn = a_near ? qa : qb, qf = a_near ? qb : qa;
+  const double E = exp(qn - qf);               // <= 1
+  const bool inside = (xa >= 0.0) && (xb >= 0.0);
+  const double Gn = inside ? exp(-qn) : 1.0;   // scale 1 inside, exp(qn) outside
+  const double ca = erfcx(fabs(xa)), cb = erfcx(fabs(xb));
+  const double cn = a_near ? ca : cb, cf = a_near ? cb : ca;
+  const double gn = Gn, gf = Gn * E;
   const double c = 0.88622692545275801365 / sk;  // sqrt(pi)/2 / sqrt(kappa)
-  double a0, gp, gm;
-  if (s0 < -1.0) {
-    const double x1 = sk * (-1.0 - s0), x2 = sk * (1.0 - s0);
-    const double e = exp((x1 - x2) * (x1 + x2));
-    a0 = c * (erfcx(x1) - erfcx(x2) * e);
-    gp = e;
-    gm = 1.0;
-  } else if (s0 > 1.0) {
-    const double x1 = sk * (s0 - 1.0), x2 = sk * (s0 + 1.0);
-    const double e = exp((x1 - x2) * (x1 + x2));
-    a0 = c * (erfcx(x1) - erfcx(x2) * e);
-    gp = 1.0;
-    gm = e;
-  } else {
-    const double up = 1.0 - s0, um = 1.0 + s0;
-    a0 = c * (erf(sk * up) + erf(sk * um));
-    gp = exp(-kap * up * up);
-    gm = exp(-kap * um * um);
-  }
-  const double inv2k = 2.0 / lam;  // 1/(2 kappa)
+  // erf(xa) + erf(xb): inside 2 - erfc(xa) - erfc(xb); outside erfc(|x_near|) - erfc(x_far)
+  const double a0 = c * (inside ? (2.0 - cn * gn - cf * gf) : (cn * gn - cf * gf));
+  const double gp = a_near ? gn : gf, gm = a_near ? gf : gn;
+  const double inv2k = 0.5 / kap;  // 1/(2 kappa)
   const double bnd_even = (gp - gm) * inv2k, bnd_odd = (gp + gm) * inv2k;
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
   J[0] = (float)a0;
@@ -169,32 +165,46 @@ __device__ __noinline__ void integrals_regime_c(double lam, double t0, float J[N
 //   g-hat = alpha + (beta-alpha) T1/T2                     eq.(29)
 // Guard (reading R7): T2 <= 0 or kappa > 1e3 -> the N = 0 value
 // alpha + (beta-alpha) I_1/I_0.
+enum Regime : int { kRegA = 0, kRegB = 1, kRegC = 2 };
+
+// a6: lambda = (beta-alpha)^2 / (2 sigma^2) (eq.(25)) and
+// theta_0 = (theta-alpha)/(beta-alpha), both rounded to fp32 (the
+// output's sensitivity to them is ~1e-5 grey), and the regime.
+__device__ __forceinline__ int range_params(float alpha, float beta, float theta, float sigma,
+                                            float& lam, float& t0) {
+  const double dd = (double)beta - (double)alpha;
+  const float d = (float)dd;
+  t0 = (float)(((double)theta - (double)alpha) / dd);
+  const float r = d / sigma;
+  lam = 0.5f * r * r;
+  if (t0 < -1.0f || t0 > 2.0f) return kRegC;
+  return (lam < (float)kLambdaSmall) ? kRegB : kRegA;
+}
+
 template <int N>
-__device__ __forceinline__ PixelResult ghat_from_nu(const float nu[N + 1], float alpha, float beta,
-                                                    float theta, float sigma, float n,
-                                                    unsigned flags) {
+__device__ __forceinline__ PixelResult ghat_from_record(const float nu[N + 1], float lam, float t0,
+                                                        float alpha, float beta, int regime,
+                                                        unsigned flags, bool want_t2n, float n) {
   PixelResult res;
   res.code = 0u;
-  const double da = (double)alpha, db = (double)beta;
-  const double dd = db - da;
-  const double t0 = ((double)theta - da) / dd;            // theta_0(i)
-  const double lam = dd * dd / (2.0 * (double)sigma * (double)sigma);  // eq.(25)
   float J[N + 2];
-  double scale_log = 0.0;  // log of the common factor applied to J (for diagnostics)
-  if (t0 < -1.0 || t0 > 2.0) {
-    integrals_regime_c<N>(lam, t0, J);
-    res.code |= kCodeFarTheta;
-    const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
-    scale_log = lam * dist * dist;
-  } else if (lam < kLambdaSmall) {
-    integrals_regime_b<N>((float)lam, (float)t0, J);
+  double scale_log = 0.0;  // log of the common factor applied to J (diagnostics only)
+  if (regime == kRegA) {
+    integrals_regime_a<N>(lam, t0, J);
+    if (want_t2n) {
+      const double sk = (double)sqrtf(0.25f * lam), s0 = 2.0 * (double)t0 - 1.0;
+      const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
+      scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
+      scale_log += 0.69314718055994530942;  // a_k = 2 J_k
+    }
+  } else if (regime == kRegB) {
+    integrals_regime_b<N>(lam, t0, J);
     res.code |= kCodeSmallLambda;
   } else {
-    integrals_regime_a<N>(lam, t0, J);
-    const double dist = t0 < 0.0 ? -t0 : (t0 > 1.0 ? t0 - 1.0 : 0.0);
-    scale_log = lam * dist * dist;
-    // regime A's J are 2x the integrals (a_k = 2 J_k)
-    scale_log += 0.69314718055994530942;
+    integrals_regime_c<N>((double)lam, (double)t0, J);
+    res.code |= kCodeFarTheta;
+    const double dist = t0 < 0.0f ? -(double)t0 : (double)t0 - 1.0;
+    scale_log = (double)lam * dist * dist;
   }
   float T2 = 0.0f, U = 0.0f, ab = 0.0f;
 #pragma unroll
@@ -213,12 +223,29 @@ __device__ __forceinline__ PixelResult ghat_from_nu(const float nu[N + 1], float
     ratio = U / T2;
   }
   res.kappa = (T2 > 0.0f) ? ab / T2 : CUDART_INF_F;
-  res.t2n = (float)((double)T2 / (double)n * exp(-scale_log));
-  const double mid = 0.5 * (da + db), half = 0.5 * dd;
+  res.t2n = want_t2n ? (float)((double)T2 / (double)n * exp(-scale_log)) : 0.0f;
+  const double da = (double)alpha, db = (double)beta;
+  const double mid = 0.5 * (da + db), half = 0.5 * (db - da);
   float g = (float)fma(half, (double)ratio, mid);
   if (flags & kFlagClamp) g = fminf(fmaxf(g, alpha), beta);
   res.g = g;
   return res;
+}
+
+// Legendre polynomial coefficients on [-1,1] as compile-time constants
+// (dyadic rationals, exact in fp64 and encodable as instruction immediates):
+// P_k(w) = 2^-k sum_m (-1)^m C(k,m) C(2k-2m,k) w^{k-2m}.
+__host__ __device__ constexpr double binom_c(int n, int k) {
+  double c = 1.0;
+  for (int i = 1; i <= k; ++i) c = c * (double)(n - k + i) / (double)i;
+  return c;
+}
+__host__ __device__ constexpr double leg_coef(int k, int r) {
+  if (r > k || ((k - r) & 1)) return 0.0;
+  const int m = (k - r) / 2;
+  double v = binom_c(k, m) * binom_c(2 * k - 2 * m, k);
+  for (int i = 0; i < k; ++i) v *= 0.5;
+  return (m & 1) ? -v : v;
 }
 
 // a4 + a5: from window power sums in tile units to Legendre moments.
@@ -233,7 +260,7 @@ template <int N>
 __device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double bu, float nu[N + 1],
                                              float flag_bits) {
   const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
-  const float ratio = (float)((1.0 + fabs(m)) / h);
+  const float ratio = (float)(1.0 + fabs(m)) / (float)h;
   if ((float)N * __log2f(ratio) > flag_bits) return false;
 #pragma unroll
   for (int i = 1; i <= N; ++i) {
@@ -251,7 +278,7 @@ __device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double 
   for (int k = 0; k <= N; ++k) {
     double v = 0.0;
 #pragma unroll
-    for (int r = k & 1; r <= k; r += 2) v = fma(c_leg[k][r], S[r], v);
+    for (int r = k & 1; r <= k; r += 2) v = fma(leg_coef(k, r), S[r], v);
     nu[k] = (float)v;
   }
   return true;
