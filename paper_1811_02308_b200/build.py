@@ -9,7 +9,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "fabf.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", "fabf_device.cuh"), os.path.join(ROOT, "include", "fabf.h")]
+DEPS = SRC + [os.path.join(PKG, "csrc", "fabf_device.cuh"), os.path.join(PKG, "csrc", "fabf_erfcx.cuh"),
+        os.path.join(ROOT, "include", "fabf.h")]
 LIB = os.path.join(PKG, "libfabf.so")
 
 NVCC_FLAGS = [

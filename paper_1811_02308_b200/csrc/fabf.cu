@@ -14,6 +14,7 @@
 //       exact direct window Legendre moments (one warp per pixel).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -36,6 +37,7 @@ struct fabf_plan_s {
   float* beta = nullptr;
   float* hmin = nullptr;   // workspace: row-pass min/max
   float* hmax = nullptr;
+  float2* blkmm = nullptr;  // per 64x32 output block (min alpha, max beta)
   int* fb_count = nullptr;  // exact-moment fallback list
   int* fb_list = nullptr;
   float* h_in = nullptr;  // device staging for fabf_filter_host
@@ -46,6 +48,9 @@ struct fabf_plan_s {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef FABF_FILTER_MINB
+#define FABF_FILTER_MINB 2
+#endif
 constexpr int kMaxRho = 96;     // L = TW + 2 rho <= 256 input columns per strip
 constexpr float kFlagBits = 26.0f;
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // opt-in limit minus static shared memory
@@ -145,6 +150,7 @@ fabf_status_t ensure_tables(int dev) {
 constexpr int kRowsTX = 256;  // outputs per CTA row (rows pass)
 constexpr int kRowsRY = 4;    // rows per CTA (rows pass)
 constexpr int kColsCX = 32;   // columns per CTA (columns pass)
+constexpr int kColsTY = 64;   // output rows per CTA (columns pass)
 
 __device__ __forceinline__ float2 mm2(float2 a, float2 b) {
   return make_float2(fminf(a.x, b.x), fmaxf(a.y, b.y));
@@ -198,7 +204,9 @@ __global__ void __launch_bounds__(kThreads) k_bounds_cols(const float* __restric
                                                            const float* __restrict__ hmax, int H,
                                                            int W, int rho, int TY,
                                                            float* __restrict__ amin,
-                                                           float* __restrict__ bmax) {
+                                                           float* __restrict__ bmax,
+                                                           float2* __restrict__ blkmm) {
+  __shared__ float2 red[kThreads / 32];
   extern __shared__ float2 sm2[];
   const int w = 2 * rho + 1;
   const int x0 = blockIdx.x * kColsCX;
@@ -228,12 +236,27 @@ __global__ void __launch_bounds__(kThreads) k_bounds_cols(const float* __restric
     bufB = t;
     K *= 2;
   }
-  if (!colok) return;
-  for (int r = ty; r < nrow; r += blockDim.y) {
-    const float2 v = mm2(bufA[r * kColsCX + tx], bufA[(r + w - K) * kColsCX + tx]);
-    const size_t o = plane + (size_t)(y0 + r) * W + x;
-    amin[o] = v.x;
-    bmax[o] = v.y;
+  float2 bm = make_float2(CUDART_INF_F, -CUDART_INF_F);
+  if (colok) {
+    for (int r = ty; r < nrow; r += blockDim.y) {
+      const float2 v = mm2(bufA[r * kColsCX + tx], bufA[(r + w - K) * kColsCX + tx]);
+      const size_t o = plane + (size_t)(y0 + r) * W + x;
+      amin[o] = v.x;
+      bmax[o] = v.y;
+      bm = mm2(bm, v);
+    }
+  }
+  if (blkmm) {  // this block's (min alpha, max beta): k_filter's tile centring
+    const int t = ty * kColsCX + tx;
+    for (int off = 16; off > 0; off >>= 1)
+      bm = mm2(bm, make_float2(__shfl_xor_sync(0xffffffffu, bm.x, off),
+                               __shfl_xor_sync(0xffffffffu, bm.y, off)));
+    if ((t & 31) == 0) red[t >> 5] = bm;
+    __syncthreads();
+    if (t == 0) {
+      for (int i = 1; i < kThreads / 32; ++i) bm = mm2(bm, red[i]);
+      blkmm[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = bm;
+    }
   }
 }
 
@@ -257,7 +280,8 @@ struct FilterArgs {
   const float* alpha;
   const float* beta;
   float* out;
-  int H, W, rho, TW, SH;
+  int B, H, W, rho, TW, SH;
+  const float2* blkmm;  // per (64-row x 32-column) output block: (min alpha, max beta)
   unsigned flags;
   float flag_bits;
   int* fb_count;
@@ -278,258 +302,303 @@ struct FilterSmem {
     off += sizeof(double) * (size_t)RB * NN * 32 * E;
     vs = off;
     off += sizeof(double) * (size_t)NN * L;
+    // the pixel queue is double buffered (C2 of step s overlaps A of step s+1)
     qnu = off;
-    off += sizeof(float) * (size_t)(N + 1) * kThreads;
+    off += 2 * sizeof(float) * (size_t)(N + 1) * kThreads;
     qlam = off;
-    off += sizeof(float) * kThreads;
+    off += 2 * sizeof(float) * kThreads;
     qt0 = off;
-    off += sizeof(float) * kThreads;
+    off += 2 * sizeof(float) * kThreads;
     qal = off;
-    off += sizeof(float) * kThreads;
+    off += 2 * sizeof(float) * kThreads;
     qbe = off;
-    off += sizeof(float) * kThreads;
+    off += 2 * sizeof(float) * kThreads;
     qo = off;
-    off += sizeof(int) * kThreads;
+    off += 2 * sizeof(int) * kThreads;
     qreg = off;
-    off += sizeof(int) * kThreads;
+    off += 2 * sizeof(int) * kThreads;
     total = off;
   }
 };
 
-template <int N>
-__global__ void __launch_bounds__(kThreads, 2) k_filter(FilterArgs a) {
+template <int N, int E, int TW>
+__global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ int cntA, cntBC;
+  __shared__ int cntA[2], cntBC[2];
   __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
   constexpr int NN = N > 0 ? N : 1;
-  const int rho = a.rho, w = 2 * rho + 1, TW = a.TW;
-  const int RB = kThreads / TW;
-  const int x0 = blockIdx.x * TW;
-  const int Y0 = blockIdx.y * a.SH;
+  constexpr int RB = kThreads / TW;  // output rows per step
+  constexpr int PSQ = 32 * E;        // one (row, q) prefix row
+  const int rho = a.rho, w = 2 * rho + 1;
   const int H = a.H, W = a.W;
-  const int Y1 = min(H, Y0 + a.SH);  // output rows [Y0, Y1)
-  const int L = TW + 2 * rho;
-  const int E = (L + 31) >> 5;
-  const size_t plane = (size_t)blockIdx.z * H * W;
+  const int L = TW + 2 * rho;  // input columns of a strip, <= 32 * E (host picks E)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const FilterSmem<N> lay(L, E, w, RB);
   double* Ps = reinterpret_cast<double*>(smraw + lay.ps);  // [RB][N][32*E]
   double* Vs = reinterpret_cast<double*>(smraw + lay.vs);  // [N][L]
-  float* qnu = reinterpret_cast<float*>(smraw + lay.qnu);   // [N+1][256]
+  float* qnu = reinterpret_cast<float*>(smraw + lay.qnu);   // [2][N+1][256]
   float* qlam = reinterpret_cast<float*>(smraw + lay.qlam);
   float* qt0 = reinterpret_cast<float*>(smraw + lay.qt0);
   float* qal = reinterpret_cast<float*>(smraw + lay.qal);
   float* qbe = reinterpret_cast<float*>(smraw + lay.qbe);
   int* qo = reinterpret_cast<int*>(smraw + lay.qo);
   int* qreg = reinterpret_cast<int*>(smraw + lay.qreg);
-  const int PSQ = 32 * E;  // one (row, q) prefix row
+  const float n = (float)(w * w);
+  const bool want_t2n = a.d_t2n != nullptr;
 
-  // ---- tile-local centre c_T and power-of-two scale s_T from the bounds of
-  // ---- the tile's outputs (their windows cover exactly the tile footprint)
-  float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
-  {
-    const int ox = x0 + (tid % TW);
-    if (ox < W) {
-      for (int yy = Y0 + tid / TW; yy < Y1; yy += RB) {
-        const size_t o = plane + (size_t)yy * W + ox;
-        lmin = fminf(lmin, __ldg(a.alpha + o));
-        lmax = fmaxf(lmax, __ldg(a.beta + o));
-      }
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
-      lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-    }
-    if (lane == 0) {
-      red_min[warp] = lmin;
-      red_max[warp] = lmax;
-    }
-    __syncthreads();
-    lmin = red_min[0];
-    lmax = red_max[0];
-    for (int i = 1; i < kThreads / 32; ++i) {
-      lmin = fminf(lmin, red_min[i]);
-      lmax = fmaxf(lmax, red_max[i]);
-    }
-  }
-  const double cT = 0.5 * ((double)lmin + (double)lmax);
-  const double halfr = 0.5 * ((double)lmax - (double)lmin);
-  int e2 = 0;
-  if (halfr > 0.0) frexp(halfr, &e2);
-  const double invS = ldexp(1.0, -e2);  // 1/s_T, s_T = 2^e2 >= half range: exact scaling
-
-  // ---- column-owner state (thread c owns input column c of the strip)
+  // column-owner identity (thread c owns input column c of the strip)
   const int c = tid;
   const bool owner = c < L;
-  const int xin = reflect_index(min(x0 - rho + c, W - 1 + rho), W);
   const int pos_c = (c % E) * 32 + c / E;
-  const float* colp = a.img + plane + xin;  // this thread's input column
-
-  // prologue: rows Y0-rho .. Y0+rho-1 (no outputs yet); V starts at zero
-  if (owner) {
-    double V[NN];
-#pragma unroll
-    for (int q = 0; q < NN; ++q) V[q] = 0.0;
-    for (int yin = Y0 - rho; yin < Y0 + rho; ++yin) {
-      const float fv = __ldg(colp + (size_t)reflect_index(yin, H) * W);
-      const double u = ((double)fv - cT) * invS;
-      double pu = u;
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        V[q] += pu;
-        pu *= u;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
-  }
-
-  const float n = (float)(w * w);
+  // pixel identity within a step
   const int px_r = tid / TW, px_x = tid % TW;
   const int pos_hi = ((px_x + 2 * rho) % E) * 32 + (px_x + 2 * rho) / E;
   const int pos_lo = px_x > 0 ? ((px_x - 1) % E) * 32 + (px_x - 1) / E : 0;
-  const bool want_t2n = a.d_t2n != nullptr;
 
-  for (int Yb = Y0; Yb < Y1; Yb += RB) {
-    const int nr = min(RB, Y1 - Yb);
-    // prefetch this thread's pixel parameters (latency hidden behind A and B)
-    const int pY = Yb + px_r, pX = x0 + px_x;
-    const bool pvalid = (px_r < nr) && (pX < W);
-    const size_t po = plane + (size_t)pY * W + pX;
-    float p_al = 0.f, p_be = 0.f, p_th = 0.f, p_sg = 1.f;
-    if (pvalid) {
-      p_al = __ldg(a.alpha + po);
-      p_be = __ldg(a.beta + po);
-      p_th = __ldg(a.theta + po);
-      p_sg = __ldg(a.sigma + po);
+  // balanced static schedule: the B * nstrips * H strip-rows are split into
+  // gridDim.x contiguous chunks (one per resident CTA); a chunk is one or two
+  // vertical segments of a strip, each walked top to bottom.
+  const int nstrips = (W + TW - 1) / TW;
+  const long long U = (long long)a.B * nstrips * H;
+  const long long u0 = (long long)blockIdx.x * U / gridDim.x;
+  const long long u1 = (long long)(blockIdx.x + 1) * U / gridDim.x;
+  int step = 0;
+  for (long long u = u0; u < u1;) {
+    const long long seg = u / H;
+    const int Y0 = (int)(u - seg * H);
+    const int Y1 = (int)min((long long)H, (long long)Y0 + (u1 - u));
+    u += Y1 - Y0;
+    const int bimg = (int)(seg / nstrips), strip = (int)(seg - (long long)bimg * nstrips);
+    const int x0 = strip * TW;
+    const size_t plane = (size_t)bimg * H * W;
+
+    // ---- tile-local centre c_T and power-of-two scale s_T: min/max over the
+    // ---- segment's output blocks (their windows cover the segment footprint)
+    float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
+    {
+      const int nby = (H + kColsTY - 1) / kColsTY, nbx = (W + kColsCX - 1) / kColsCX;
+      const int by0 = Y0 / kColsTY, by1 = (Y1 - 1) / kColsTY;
+      const int bx0 = x0 / kColsCX, bx1 = min(W - 1, x0 + TW - 1) / kColsCX;
+      const int nbw = bx1 - bx0 + 1, nblk = (by1 - by0 + 1) * nbw;
+      for (int i = tid; i < nblk; i += kThreads) {
+        const int by = by0 + i / nbw, bx = bx0 + i % nbw;
+        const float2 mm = a.blkmm[((size_t)bimg * nby + by) * nbx + bx];
+        lmin = fminf(lmin, mm.x);
+        lmax = fmaxf(lmax, mm.y);
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
+        lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
+      }
+      if (lane == 0) {
+        red_min[warp] = lmin;
+        red_max[warp] = lmax;
+      }
+      __syncthreads();
+      lmin = red_min[0];
+      lmax = red_max[0];
+#pragma unroll
+      for (int i = 1; i < kThreads / 32; ++i) {
+        lmin = fminf(lmin, red_min[i]);
+        lmax = fmaxf(lmax, red_max[i]);
+      }
     }
-    if (tid == 0) {
-      cntA = 0;
-      cntBC = 0;
-    }
-    // ---- phase A
+    const double cT = 0.5 * ((double)lmin + (double)lmax);
+    const double halfr = 0.5 * ((double)lmax - (double)lmin);
+    int e2 = 0;
+    if (halfr > 0.0) frexp(halfr, &e2);
+    const double invS = ldexp(1.0, -e2);  // 1/s_T, s_T = 2^e2 >= half range: exact scaling
+
+    const int xin = reflect_index(min(x0 - rho + c, W - 1 + rho), W);
+    const float* colp = a.img + plane + xin;  // this thread's input column
+
+    // prologue: rows Y0-rho .. Y0+rho-1 (no outputs yet); V starts at zero
     if (owner) {
       double V[NN];
 #pragma unroll
-      for (int q = 0; q < N; ++q) V[q] = Vs[(size_t)q * L + c];
-      for (int r = 0; r < nr; ++r) {
-        // entering row Yb+r+rho, leaving row Yb+r-rho-1 (re-read: L2-resident)
-        const int yin = Yb + r + rho, yout = yin - w;
+      for (int q = 0; q < NN; ++q) V[q] = 0.0;
+      for (int yin = Y0 - rho; yin < Y0 + rho; ++yin) {
         const float fv = __ldg(colp + (size_t)reflect_index(yin, H) * W);
-        const bool leave = yout >= Y0 - rho;
-        const float fo = leave ? __ldg(colp + (size_t)reflect_index(yout, H) * W) : 0.0f;
         const double u = ((double)fv - cT) * invS;
-        const double uo = leave ? ((double)fo - cT) * invS : 0.0;
-        double pu = u, po2 = uo;
+        double pu = u;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
-          V[q] += pu - po2;
+          V[q] += pu;
           pu *= u;
-          po2 *= uo;
         }
-#pragma unroll
-        for (int q = 0; q < N; ++q) Ps[((size_t)r * NN + q) * PSQ + pos_c] = V[q];
       }
 #pragma unroll
       for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
     }
-    __syncthreads();
-    // ---- phase B: inclusive prefix sums over c for each (r, q)
-    if (N > 0) {
-      for (int s = warp; s < nr * N; s += kThreads / 32) {
-        double* row = Ps + (size_t)s * PSQ;
-        double loc[8];
-        double tot = 0.0;
+
+    // phase-A input prefetch: entering / leaving samples of the next step's rows
+    float pf_in[RB], pf_out[RB];
+    auto prefetch = [&](int Yb) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (e < E) tot += row[e * 32 + lane];
-          loc[e] = tot;
-        }
-        double inc = tot;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const double v = __shfl_up_sync(0xffffffffu, inc, off);
-          if (lane >= off) inc += v;
-        }
-        // exclusive offset straight from the neighbour (never inc - tot: a lane
-        // whose chunk runs into the padding carries garbage in tot)
-        double excl = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0) excl = 0.0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < E) row[e * 32 + lane] = loc[e] + excl;
+      for (int r = 0; r < RB; ++r) {
+        const int yin = Yb + r + rho, yout = yin - w;
+        const bool ok = owner && (Yb + r < Y1);
+        pf_in[r] = ok ? __ldg(colp + (size_t)reflect_index(yin, H) * W) : 0.0f;
+        pf_out[r] = (ok && yout >= Y0 - rho) ? __ldg(colp + (size_t)reflect_index(yout, H) * W) : 0.0f;
       }
-    }
-    __syncthreads();
-    // ---- phase C1: stretch + range parameters + enqueue
-    {
-      int regime = -1;  // -1: no record (invalid, identity or fallback)
-      float nu[N + 1];
-      float lam = 0.f, t0 = 0.f;
+    };
+    prefetch(Y0);
+
+    for (int Yb = Y0; Yb < Y1; Yb += RB, ++step) {
+      const int nr = min(RB, Y1 - Yb);
+      const int qb = step & 1;
+      float* qnu_b = qnu + (size_t)qb * (N + 1) * kThreads;
+      float* qlam_b = qlam + qb * kThreads;
+      float* qt0_b = qt0 + qb * kThreads;
+      float* qal_b = qal + qb * kThreads;
+      float* qbe_b = qbe + qb * kThreads;
+      int* qo_b = qo + qb * kThreads;
+      int* qreg_b = qreg + qb * kThreads;
+      // this thread's pixel parameters (latency hidden behind A and B)
+      const int pY = Yb + px_r, pX = x0 + px_x;
+      const bool pvalid = (px_r < nr) && (pX < W);
+      const size_t po = plane + (size_t)pY * W + pX;
+      float p_al = 0.f, p_be = 0.f, p_th = 0.f, p_sg = 1.f;
       if (pvalid) {
-        if (p_al == p_be) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
-          a.out[po] = p_al;
-          if (a.d_kappa) a.d_kappa[po] = 1.0f;
-          if (a.d_t2n) a.d_t2n[po] = 1.0f;
-          if (a.d_code) a.d_code[po] = (unsigned char)kCodeIdentity;
-        } else {
-          double S[N + 1];
-          S[0] = (double)n;
+        p_al = __ldg(a.alpha + po);
+        p_be = __ldg(a.beta + po);
+        p_th = __ldg(a.theta + po);
+        p_sg = __ldg(a.sigma + po);
+      }
+      if (tid == 0) {
+        cntA[qb] = 0;
+        cntBC[qb] = 0;
+      }
+      // ---- phase A: entering row Yb+r+rho in, leaving row Yb+r-rho-1 out
+      if (owner) {
+        float fin[RB], fout[RB];
 #pragma unroll
-          for (int q = 1; q <= N; ++q) {
-            const double* row = Ps + ((size_t)px_r * NN + (q - 1)) * PSQ;
-            S[q] = row[pos_hi] - (px_x > 0 ? row[pos_lo] : 0.0);
-          }
-          const double au = ((double)p_al - cT) * invS, bu = ((double)p_be - cT) * invS;
-          if (nu_from_sums<N>(S, au, bu, nu, a.flag_bits)) {
-            regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
-          } else {  // exact-moment fallback pass writes this pixel
-            const int slotfb = atomicAdd(a.fb_count, 1);
-            a.fb_list[slotfb] = (int)po;
+        for (int r = 0; r < RB; ++r) {
+          fin[r] = pf_in[r];
+          fout[r] = pf_out[r];
+        }
+        prefetch(Yb + RB);
+        double V[NN];
+#pragma unroll
+        for (int q = 0; q < N; ++q) V[q] = Vs[(size_t)q * L + c];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          if (r < nr) {
+            // before the window is full the leaving sample contributes u_o = 0
+            const bool leave = Yb + r - rho - 1 >= Y0 - rho;
+            const double u = ((double)fin[r] - cT) * invS;
+            const double uo = leave ? ((double)fout[r] - cT) * invS : 0.0;
+            double pu = u, po2 = uo;
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+              V[q] += pu - po2;
+              pu *= u;
+              po2 *= uo;
+            }
+#pragma unroll
+            for (int q = 0; q < N; ++q) Ps[(r * NN + q) * PSQ + pos_c] = V[q];
           }
         }
-      }
-      const unsigned mA = __ballot_sync(0xffffffffu, regime == kRegA);
-      const unsigned mB = __ballot_sync(0xffffffffu, regime > kRegA);
-      int baseA = 0, baseB = 0;
-      if (lane == 0) {
-        if (mA) baseA = atomicAdd(&cntA, __popc(mA));
-        if (mB) baseB = atomicAdd(&cntBC, __popc(mB));
-      }
-      baseA = __shfl_sync(0xffffffffu, baseA, 0);
-      baseB = __shfl_sync(0xffffffffu, baseB, 0);
-      const unsigned lt = (1u << lane) - 1u;
-      if (regime >= 0) {
-        const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
-                                        : kThreads - 1 - (baseB + __popc(mB & lt));
 #pragma unroll
-        for (int k = 0; k <= N; ++k) qnu[k * kThreads + j] = nu[k];
-        qlam[j] = lam;
-        qt0[j] = t0;
-        qal[j] = p_al;
-        qbe[j] = p_be;
-        qo[j] = (int)po;
-        qreg[j] = regime;
+        for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
       }
-    }
-    __syncthreads();
-    // ---- phase C2: integrals, ratio, guard, store (one regime per warp)
-    {
-      const int j = tid;
-      if (j < cntA || j >= kThreads - cntBC) {
+      __syncthreads();
+      // ---- phase B: inclusive prefix sums over c for each (r, q), a warp each
+      if (N > 0) {
+        for (int s = warp; s < nr * N; s += kThreads / 32) {
+          double* row = Ps + s * PSQ + lane;
+          double loc[E];
+          double tot = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            tot += row[e * 32];
+            loc[e] = tot;
+          }
+          double inc = tot;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double v = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += v;
+          }
+          // exclusive offset straight from the neighbour (never inc - tot: a lane
+          // whose chunk runs into the padding carries garbage in tot)
+          double excl = __shfl_up_sync(0xffffffffu, inc, 1);
+          if (lane == 0) excl = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) row[e * 32] = loc[e] + excl;
+        }
+      }
+      __syncthreads();
+      // ---- phase C1: stretch + range parameters + enqueue
+      {
+        int regime = -1;  // -1: no record (invalid, identity or fallback)
         float nu[N + 1];
+        float lam = 0.f, t0 = 0.f;
+        if (pvalid) {
+          if (p_al == p_be) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
+            a.out[po] = p_al;
+            if (a.d_kappa) a.d_kappa[po] = 1.0f;
+            if (a.d_t2n) a.d_t2n[po] = 1.0f;
+            if (a.d_code) a.d_code[po] = (unsigned char)kCodeIdentity;
+          } else {
+            double S[N + 1];
+            S[0] = (double)n;
 #pragma unroll
-        for (int k = 0; k <= N; ++k) nu[k] = qnu[k * kThreads + j];
-        const int o = qo[j];
-        PixelResult res = ghat_from_record<N>(nu, qlam[j], qt0[j], qal[j], qbe[j], qreg[j],
-                                              a.flags, want_t2n, n);
-        a.out[o] = res.g;
-        if (a.d_kappa) a.d_kappa[o] = res.kappa;
-        if (a.d_t2n) a.d_t2n[o] = res.t2n;
-        if (a.d_code) a.d_code[o] = (unsigned char)res.code;
+            for (int q = 1; q <= N; ++q) {
+              const double* row = Ps + (px_r * NN + (q - 1)) * PSQ;
+              S[q] = row[pos_hi] - (px_x > 0 ? row[pos_lo] : 0.0);
+            }
+            const double au = ((double)p_al - cT) * invS, bu = ((double)p_be - cT) * invS;
+            if (nu_from_sums<N>(S, au, bu, nu, a.flag_bits)) {
+              regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
+            } else {  // exact-moment fallback pass writes this pixel
+              const int slotfb = atomicAdd(a.fb_count, 1);
+              a.fb_list[slotfb] = (int)po;
+            }
+          }
+        }
+        const unsigned mA = __ballot_sync(0xffffffffu, regime == kRegA);
+        const unsigned mB = __ballot_sync(0xffffffffu, regime > kRegA);
+        int baseA = 0, baseB = 0;
+        if (lane == 0) {
+          if (mA) baseA = atomicAdd(&cntA[qb], __popc(mA));
+          if (mB) baseB = atomicAdd(&cntBC[qb], __popc(mB));
+        }
+        baseA = __shfl_sync(0xffffffffu, baseA, 0);
+        baseB = __shfl_sync(0xffffffffu, baseB, 0);
+        const unsigned lt = (1u << lane) - 1u;
+        if (regime >= 0) {
+          const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
+                                          : kThreads - 1 - (baseB + __popc(mB & lt));
+#pragma unroll
+          for (int k = 0; k <= N; ++k) qnu_b[k * kThreads + j] = nu[k];
+          qlam_b[j] = lam;
+          qt0_b[j] = t0;
+          qal_b[j] = p_al;
+          qbe_b[j] = p_be;
+          qo_b[j] = (int)po;
+          qreg_b[j] = regime;
+        }
+      }
+      __syncthreads();
+      // ---- phase C2: integrals, ratio, guard, store (one regime per warp).  No
+      // ---- barrier after it: the queue and its counters are double buffered.
+      {
+        const int j = tid;
+        if (j < cntA[qb] || j >= kThreads - cntBC[qb]) {
+          float nu[N + 1];
+#pragma unroll
+          for (int k = 0; k <= N; ++k) nu[k] = qnu_b[k * kThreads + j];
+          const int o = qo_b[j];
+          PixelResult res = ghat_from_record<N>(nu, qlam_b[j], qt0_b[j], qal_b[j], qbe_b[j],
+                                                qreg_b[j], a.flags, want_t2n, n);
+          a.out[o] = res.g;
+          if (a.d_kappa) a.d_kappa[o] = res.kappa;
+          if (a.d_t2n) a.d_t2n[o] = res.t2n;
+          if (a.d_code) a.d_code[o] = (unsigned char)res.code;
+        }
       }
     }
-    __syncthreads();
   }
 }
 
@@ -628,7 +697,7 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
   k_bounds_rows<<<g1, kThreads, smem_rows, st>>>(img, p->H, p->W, rho, p->hmin, p->hmax);
   FABF_CUDA(cudaGetLastError(), "k_bounds_rows launch");
   prof_mark(1, st);
-  const int TY = 64;
+  const int TY = kColsTY;
   const size_t smem_cols = sizeof(float2) * 2 * (TY + 2 * rho) * kColsCX;
   static bool attr_set = false;
   if (!attr_set) {
@@ -639,27 +708,54 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
   }
   dim3 g2((p->W + kColsCX - 1) / kColsCX, (p->H + TY - 1) / TY, p->B);
   k_bounds_cols<<<g2, dim3(kColsCX, kThreads / kColsCX), smem_cols, st>>>(
-      p->hmin, p->hmax, p->H, p->W, rho, TY, alpha, beta);
+      p->hmin, p->hmax, p->H, p->W, rho, TY, alpha, beta, p->blkmm);
   FABF_CUDA(cudaGetLastError(), "k_bounds_cols launch");
   prof_mark(2, st);
   return FABF_OK;
 }
 
-template <int N>
-fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
-  const int L = fa.TW + 2 * fa.rho, w = 2 * fa.rho + 1, RB = kThreads / fa.TW;
-  const size_t smem = FilterSmem<N>(L, (L + 31) / 32, w, RB).total;
-  static bool attr_set = false;
-  if (!attr_set) {
-    FABF_CUDA(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int N, int E, int TW>
+fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
+  const int L = TW + 2 * fa.rho, w = 2 * fa.rho + 1, RB = kThreads / TW;
+  const size_t smem = FilterSmem<N>(L, E, w, RB).total;
+  if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
+  static int grid_cache[64] = {};  // resident CTAs per device (persistent schedule)
+  static size_t smem_cache[64] = {};
+  int dev = 0;
+  FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (grid_cache[dev] == 0 || smem_cache[dev] != smem) {
+    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxDynSmem),
               "cudaFuncSetAttribute(k_filter)");
-    attr_set = true;
+    int per_sm = 0, sms = 0;
+    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW>, kThreads, smem),
+              "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    FABF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    grid_cache[dev] = max(1, per_sm) * sms;
+    smem_cache[dev] = smem;
   }
-  if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
-  dim3 grid((fa.W + fa.TW - 1) / fa.TW, (fa.H + fa.SH - 1) / fa.SH, B);
-  k_filter<N><<<grid, kThreads, smem, st>>>(fa);
+  const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * fa.H;
+  const int grid = (int)std::min<long long>(grid_cache[dev], strips);
+  k_filter<N, E, TW><<<grid, kThreads, smem, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
+  return FABF_OK;
+}
+
+template <int N>
+fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
+  (void)B;
+  const int L128 = 128 + 2 * fa.rho;
+  fabf_status_t s;
+  if (L128 <= 128)
+    s = launch_filter_net<N, 4, 128>(fa, st);
+  else if (L128 <= 192)
+    s = launch_filter_net<N, 6, 128>(fa, st);
+  else if (L128 <= 256)
+    s = launch_filter_net<N, 8, 128>(fa, st);
+  else
+    s = launch_filter_net<N, 8, 64>(fa, st);
+  if (s != FABF_OK) return s;
   prof_mark(3, st);
   k_fallback<N><<<148 * 2, kThreads, 0, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_fallback launch");
@@ -725,8 +821,10 @@ fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const f
   fa.H = p->H;
   fa.W = p->W;
   fa.rho = rho;
+  fa.B = p->B;
   fa.TW = (rho <= 64) ? 128 : 64;
-  fa.SH = 128;
+  fa.SH = 0;  // unused: persistent balanced schedule
+  fa.blkmm = p->blkmm;
   fa.flags = p->flags;
   fa.flag_bits = kFlagBits;
   fa.fb_count = p->fb_count;
@@ -769,6 +867,8 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
       (e = cudaMalloc(&p->beta, px * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&p->hmin, px * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&p->hmax, px * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&p->blkmm, sizeof(float2) * (size_t)batch * ((height + kColsTY - 1) / kColsTY) *
+                                     ((width + kColsCX - 1) / kColsCX))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_count, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess) {
     fabf_destroy(p);
@@ -867,6 +967,7 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   cudaFree(p->beta);
   cudaFree(p->hmin);
   cudaFree(p->hmax);
+  cudaFree(p->blkmm);
   cudaFree(p->fb_count);
   cudaFree(p->fb_list);
   cudaFree(p->h_in);

@@ -8,6 +8,7 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+
 namespace fabf {
 
 constexpr int kMaxN = 10;
@@ -33,6 +34,57 @@ __constant__ float c_glB_W[kMaxN + 2][kGlB];
 // Regime C: 24-node Gauss-Legendre nodes / weights on [0,1] (fp64).
 __constant__ double c_glC_x[kGlC];
 __constant__ double c_glC_w[kGlC];
+
+// Estrin evaluation of sum_{j=LO}^{HI} c[j] x^(j-LO), pw[l] = x^(2^l): the
+// dependency depth is ~log2(terms) instead of Horner's (terms - 1), which is
+// what matters in this latency-bound kernel.
+__host__ __device__ constexpr int estrin_split(int n) {
+  int h = 1;
+  while (2 * h < n) h *= 2;
+  return h;
+}
+__host__ __device__ constexpr int ilog2c(int n) {
+  int l = 0;
+  while ((1 << (l + 1)) <= n) ++l;
+  return l;
+}
+template <int LO, int HI>
+__device__ __forceinline__ double estrin(const double* c, const double* pw) {
+  constexpr int n = HI - LO + 1;
+  if constexpr (n == 1) {
+    return c[LO];
+  } else {
+    constexpr int h = estrin_split(n);
+    return fma(estrin<LO + h, HI>(c, pw), pw[ilog2c(h)], estrin<LO, LO + h - 1>(c, pw));
+  }
+}
+template <int DEG>
+__device__ __forceinline__ double poly_estrin(const double* c, double x) {
+  double pw[5];
+  pw[0] = x;
+#pragma unroll
+  for (int l = 1; l < 5; ++l) pw[l] = pw[l - 1] * pw[l - 1];
+  return estrin<0, DEG>(c, pw);
+}
+
+// exp(z) for z <= 0 in fp64 (z < -708 gives 0): Cody-Waite reduction by ln 2
+// (hi/lo split), degree-12 Taylor polynomial on |r| <= ln2/2 (truncation
+// < 2e-16), 2^k built in the exponent field.  Branch-free; coefficients in
+// constant memory so DFMA reads them as c[] operands.
+__constant__ double c_exp_poly[13] = {
+    1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
+    1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600};
+__device__ __forceinline__ double exp_nonpos(double z) {
+  const double kd = rint(z * 1.4426950408889634074);
+  double r = fma(kd, -6.93147180369123816490e-01, z);
+  r = fma(kd, -1.90821492927058770002e-10, r);
+  const double p = poly_estrin<12>(c_exp_poly, r);
+  const long long k = (long long)kd;
+  const double scale = __longlong_as_double((k + 1023) << 52);
+  return (z < -708.0) ? 0.0 : p * scale;
+}
+
+#include "fabf_erfcx.cuh"
 
 struct PixelResult {
   float g;
@@ -68,10 +120,10 @@ __device__ __forceinline__ void integrals_regime_a(float lam, float t0, float J[
   const double qa = xa * xa, qb = xb * xb;
   const bool a_near = qa < qb;
   const double qn = a_near ? qa : qb, qf = a_near ? qb : qa;
-  const double E = exp(qn - qf);               // <= 1
+  const double E = exp_nonpos(qn - qf);        // <= 1
   const bool inside = (xa >= 0.0) && (xb >= 0.0);
-  const double Gn = inside ? exp(-qn) : 1.0;   // scale 1 inside, exp(qn) outside
-  const double ca = erfcx(fabs(xa)), cb = erfcx(fabs(xb));
+  const double Gn = inside ? exp_nonpos(-qn) : 1.0;  // scale 1 inside, exp(qn) outside
+  const double ca = erfcx_pos(fabs(xa)), cb = erfcx_pos(fabs(xb));
   const double cn = a_near ? ca : cb, cf = a_near ? cb : ca;
   const double gn = Gn, gf = Gn * E;
   const double c = 0.88622692545275801365 / sk;  // sqrt(pi)/2 / sqrt(kappa)
@@ -172,10 +224,9 @@ enum Regime : int { kRegA = 0, kRegB = 1, kRegC = 2 };
 // output's sensitivity to them is ~1e-5 grey), and the regime.
 __device__ __forceinline__ int range_params(float alpha, float beta, float theta, float sigma,
                                             float& lam, float& t0) {
-  const double dd = (double)beta - (double)alpha;
-  const float d = (float)dd;
-  t0 = (float)(((double)theta - (double)alpha) / dd);
-  const float r = d / sigma;
+  const float d = (float)((double)beta - (double)alpha);
+  t0 = __fdividef((float)((double)theta - (double)alpha), d);
+  const float r = __fdividef(d, sigma);
   lam = 0.5f * r * r;
   if (t0 < -1.0f || t0 > 2.0f) return kRegC;
   return (lam < (float)kLambdaSmall) ? kRegB : kRegA;

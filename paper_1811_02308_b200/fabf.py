@@ -12,7 +12,7 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_PKG, "libfabf.so")
+library_path = os.environ.get("FABF_LIB") or os.path.join(_PKG, "libfabf.so")  # FABF_LIB: experiments
 
 FLAG_LITERAL = 0x1
 FLAG_CLAMP = 0x2
