@@ -52,30 +52,38 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.path = None
 
     def __enter__(self):
+        import tempfile
+
         try:
+            fd, self.path = tempfile.mkstemp(prefix="fabf_clocks_", suffix=".csv")
+            self.fh = os.fdopen(fd, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.fh, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
         if self.proc is not None:
+            time.sleep(0.2)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.fh.close()
+            try:
+                with open(self.path) as f:
+                    self.lines = [ln.strip() for ln in f]
+                os.unlink(self.path)
+            except Exception:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
@@ -96,6 +104,26 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+# B200 FP64 pipe: 64 FMA/clk/SM (microbench: 1.71e13 FMA/s at the clocks seen,
+# profiles/r1_microbench.json) x 148 SMs x 1.965 GHz max clock x 2 flop/FMA.
+FP64_PEAK_TFLOPS = 64 * 148 * 1.965e9 * 2 / 1e12  # 37.2, derived from unit counts and clocks
+
+
+def fp64_flops_per_pixel(N: int) -> int:
+    """Algorithmic fp64 flops per pixel of the dominant kernel (FMA = 2 flops),
+    counted from the method's steps as implemented (DESIGN.md section 4,
+    'Roofline'); halo and prologue recomputation are NOT counted.
+      a3 moments  : entering + leaving sample 2*(2 + (N-1) + N), prefix + difference 2N
+      a4 stretch  : Taylor shift N(N+1)/2 FMA, scaling 2N-1, Legendre sum_k (k//2+1) FMA
+      a7 regime A : 2 erfcx (20 FMA + 2), 2 exp (14 FMA + 1), seeds 10,
+                    recurrence (N+1) * (3 FMA + 1 MUL)
+    """
+    a3 = 2 * (2 + (N - 1) + N) + 2 * N
+    a4 = N * (N + 1) + (2 * N - 1) + 2 * sum(k // 2 + 1 for k in range(N + 1))
+    a7 = 2 * (2 * 20 + 2) + 2 * (2 * 14 + 1) + 10 + (N + 1) * (3 * 2 + 1)
+    return a3 + a4 + a7
 
 
 def _dist():
@@ -183,12 +211,13 @@ def run_gpu(args):
     def step():
         fb.filter(plan, img, th, sg, w.rho, w.N, out=out)
 
+    clk = ClockSampler(local).__enter__()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    if True:
         if ws > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -211,6 +240,7 @@ def run_gpu(args):
         _, ms4 = fb.filter_profile(plan, img, th, sg, w.rho, w.N, out=out)
         stage += np.array(ms4)
     stage /= args.steps
+    clk.__exit__(None, None, None)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
     h_img = torch.from_numpy(w.img).pin_memory()
@@ -238,7 +268,14 @@ def run_gpu(args):
         alg_bytes = 16.0 * px  # f, theta, sigma read + g written, fp32
         hbm = {"bound": "hbm", "achieved": alg_bytes / (ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                "unit": "GB/s", "frac": alg_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-               "traffic": None, "peak_source": peak_src}
+               "traffic": None, "peak_source": peak_src, "scope": "whole step, 16 B/px"}
+        kf_ms = float(stage[2])  # dominant kernel k_filter, CUDA events on the launch stream
+        flops = fp64_flops_per_pixel(w.N) * px
+        fp64 = {"bound": "alu", "pipe": "fp64", "achieved": flops / (kf_ms * 1e-3) / 1e12,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": flops / (kf_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                "traffic": None, "kernel": "k_filter", "kernel_ms": kf_ms,
+                "flops_per_pixel": fp64_flops_per_pixel(w.N),
+                "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz x 2 (microbench measured 34.2 TF/s)"}
         line = {
             "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -246,7 +283,8 @@ def run_gpu(args):
             "config": {"workload": w.name, "height": H, "width": W, "rho": w.rho, "N": w.N,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"{ws} independent frames (one per GPU)" if ws > 1 else "1 GPU"},
-            "roofline": hbm,
+            "roofline": fp64,
+            "hbm_roofline": hbm,
             "step_ms": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms)},
             "fallback_pixels": fallback,
             "stage_ms": {"bounds_rows": stage[0], "bounds_cols": stage[1], "filter": stage[2],
