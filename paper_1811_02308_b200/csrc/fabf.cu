@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds_cols(const float* __restric
 //      to / remove the leaving row's powers from their fp64 vertical sums V_q
 //      (kept in shared memory between steps) and write them to Ps;
 //   B  one warp per (row, q): inclusive prefix scan of Ps along the strip
-//      (lane-transposed layout pos(c) = (c % E)*32 + c / E: conflict-free);
+//      (natural layout, lane l owns entries [lE, lE+E) with E odd: conflict-free);
 //   C1 one pixel per thread: window sums = prefix differences, stretch to
 //      Legendre moments (fp64), range parameters, regime; the record goes to a
 //      shared-memory queue, regime-A records from the front, B/C from the back;
@@ -349,11 +349,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   // column-owner identity (thread c owns input column c of the strip)
   const int c = tid;
   const bool owner = c < L;
-  const int pos_c = (c % E) * 32 + c / E;
+  const int pos_c = c;  // natural layout; phase B lanes own E (odd) consecutive entries
   // pixel identity within a step
   const int px_r = tid / TW, px_x = tid % TW;
-  const int pos_hi = ((px_x + 2 * rho) % E) * 32 + (px_x + 2 * rho) / E;
-  const int pos_lo = px_x > 0 ? ((px_x - 1) % E) * 32 + (px_x - 1) / E : 0;
+  const int pos_hi = px_x + 2 * rho;
+  const int pos_lo = px_x > 0 ? px_x - 1 : 0;
 
   // balanced static schedule: the B * nstrips * H strip-rows are split into
   // gridDim.x contiguous chunks (one per resident CTA); a chunk is one or two
@@ -503,29 +503,46 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
       }
       __syncthreads();
-      // ---- phase B: inclusive prefix sums over c for each (r, q), a warp each
+      // ---- phase B: inclusive prefix sums over c for each (r, q).  Lane l owns
+      // ---- entries [l*E, l*E+E): with E odd the 8-byte accesses of a warp hit
+      // ---- distinct bank pairs (conflict-free); two scans per warp interleaved.
       if (N > 0) {
-        for (int s = warp; s < nr * N; s += kThreads / 32) {
-          double* row = Ps + s * PSQ + lane;
-          double loc[E];
-          double tot = 0.0;
+        constexpr int NW = kThreads / 32;
+        for (int s0 = warp; s0 < nr * N; s0 += 2 * NW) {
+          const int s1 = s0 + NW;
+          const bool two = s1 < nr * N;
+          double* row0 = Ps + s0 * PSQ + lane * E;
+          double* row1 = Ps + (two ? s1 : s0) * PSQ + lane * E;
+          double loc0[E], loc1[E];
+          double tot0 = 0.0, tot1 = 0.0;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            tot += row[e * 32];
-            loc[e] = tot;
+            tot0 += row0[e];
+            tot1 += row1[e];
+            loc0[e] = tot0;
+            loc1[e] = tot1;
           }
-          double inc = tot;
+          double inc0 = tot0, inc1 = tot1;
 #pragma unroll
           for (int off = 1; off < 32; off <<= 1) {
-            const double v = __shfl_up_sync(0xffffffffu, inc, off);
-            if (lane >= off) inc += v;
+            const double v0 = __shfl_up_sync(0xffffffffu, inc0, off);
+            const double v1 = __shfl_up_sync(0xffffffffu, inc1, off);
+            if (lane >= off) {
+              inc0 += v0;
+              inc1 += v1;
+            }
           }
-          // exclusive offset straight from the neighbour (never inc - tot: a lane
-          // whose chunk runs into the padding carries garbage in tot)
-          double excl = __shfl_up_sync(0xffffffffu, inc, 1);
-          if (lane == 0) excl = 0.0;
+          // exclusive offsets straight from the neighbour (never inc - tot: a
+          // lane whose chunk runs into the padding carries garbage in tot)
+          double ex0 = __shfl_up_sync(0xffffffffu, inc0, 1);
+          double ex1 = __shfl_up_sync(0xffffffffu, inc1, 1);
+          if (lane == 0) ex0 = ex1 = 0.0;
 #pragma unroll
-          for (int e = 0; e < E; ++e) row[e * 32] = loc[e] + excl;
+          for (int e = 0; e < E; ++e) row0[e] = loc0[e] + ex0;
+          if (two) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) row1[e] = loc1[e] + ex1;
+          }
         }
       }
       __syncthreads();
@@ -747,14 +764,15 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   (void)B;
   const int L128 = 128 + 2 * fa.rho;
   fabf_status_t s;
-  if (L128 <= 128)
-    s = launch_filter_net<N, 4, 128>(fa, st);
-  else if (L128 <= 192)
-    s = launch_filter_net<N, 6, 128>(fa, st);
+  // prefix rows of 32*E doubles, E odd (conflict-free strided phase-B access)
+  if (L128 <= 160)
+    s = launch_filter_net<N, 5, 128>(fa, st);
+  else if (L128 <= 224)
+    s = launch_filter_net<N, 7, 128>(fa, st);
   else if (L128 <= 256)
-    s = launch_filter_net<N, 8, 128>(fa, st);
+    s = launch_filter_net<N, 9, 128>(fa, st);
   else
-    s = launch_filter_net<N, 8, 64>(fa, st);
+    s = launch_filter_net<N, 9, 64>(fa, st);
   if (s != FABF_OK) return s;
   prof_mark(3, st);
   k_fallback<N><<<148 * 2, kThreads, 0, st>>>(fa);
