@@ -35,9 +35,7 @@ struct fabf_plan_s {
   int device = 0;
   float* alpha = nullptr;  // workspace: bounds
   float* beta = nullptr;
-  float* hmin = nullptr;   // workspace: row-pass min/max
-  float* hmax = nullptr;
-  float2* blkmm = nullptr;  // per 64x32 output block (min alpha, max beta)
+  float2* blkmm = nullptr;  // per bounds tile (min alpha, max beta)
   int* fb_count = nullptr;  // exact-moment fallback list
   int* fb_list = nullptr;
   float* h_in = nullptr;  // device staging for fabf_filter_host
@@ -141,119 +139,184 @@ fabf_status_t ensure_tables(int dev) {
 }  // namespace
 
 // ============================================================================
-// step a1: bounds (eq.(8)) -- separable sliding min/max, one pass per
-// direction, each by log-doubling in shared memory: M_1 = f,
-// M_2j(x) = op(M_j(x), M_j(x+j)); the window [x, x+w-1] is
-// op(M_K(x), M_K(x+w-K)) with K the largest power of two <= w.  ceil(log2 w)
-// comparisons per sample and pass, independent of the image content; min and
-// max travel together as float2.  Comparisons only: bit-exact.
-constexpr int kRowsTX = 256;  // outputs per CTA row (rows pass)
-constexpr int kRowsRY = 4;    // rows per CTA (rows pass)
-constexpr int kColsCX = 32;   // columns per CTA (columns pass)
-constexpr int kColsTY = 64;   // output rows per CTA (columns pass)
+// step a1: bounds (eq.(8)) -- one CTA per kBT x kBT output tile,
+// separable sliding min/max by van Herk / Gil-Werman (the O(1) MAX-FILTER of
+// Prop.1), both passes in one kernel:
+//   pass V: walkers = (footprint column, row segment); inputs straight from
+//           global memory (lanes = adjacent columns: coalesced), results into
+//           shared Vm[kBT][P] (P = kBT + 2 rho, odd pitch);
+//   pass H: walkers = (output row, column segment) over Vm, results into
+//           shared O[kBT][kBT + 1], then copied out coalesced as alpha, beta,
+//           together with the tile's (min alpha, max beta) for k_filter.
+// A walker with outputs o = 0..len-1 over inputs in(0 .. len + 2 rho - 1) cuts
+// the inputs into blocks of w = 2 rho + 1 aligned at 0; for o in block b
+//   out(o) = op(h(o), g(o + w - 1)),
+// h = suffix op within block b (backward sweep, stored in the output slot),
+// g = prefix op within block b + 1 (running register, empty at o = b w).
+// 3 comparisons per sample and pass whatever rho is; comparisons only: exact.
+constexpr int kBT = 64;    // bounds tile side (output rows and columns)
+constexpr int kBSegV = 32;  // pass-V segment length (rows)
+constexpr int kBSegH = 16;  // pass-H segment length (columns)
 
 __device__ __forceinline__ float2 mm2(float2 a, float2 b) {
   return make_float2(fminf(a.x, b.x), fmaxf(a.y, b.y));
 }
 
-__global__ void __launch_bounds__(kThreads) k_bounds_rows(const float* __restrict__ img, int H,
-                                                           int W, int rho,
-                                                           float* __restrict__ hmin,
-                                                           float* __restrict__ hmax) {
-  extern __shared__ float2 sm2[];
-  const int w = 2 * rho + 1;
-  const int LS = kRowsTX + 2 * kMaxRho;  // row stride of the staging buffers
-  const int x0 = blockIdx.x * kRowsTX;
-  const int y0 = blockIdx.y * kRowsRY;
-  const size_t plane = (size_t)blockIdx.z * H * W;
-  const int nout = min(kRowsTX, W - x0);
-  const int nrow = min(kRowsRY, H - y0);
-  const int L = nout + 2 * rho;
-  float2* bufA = sm2;
-  float2* bufB = sm2 + kRowsRY * LS;
-  for (int i = threadIdx.x; i < nrow * L; i += blockDim.x) {
-    const int r = i / L, c = i - r * L;
-    const float v = __ldg(img + plane + (size_t)(y0 + r) * W + reflect_index(x0 - rho + c, W));
-    bufA[r * LS + c] = make_float2(v, v);
-  }
-  __syncthreads();
-  int K = 1;
-  while (2 * K <= w) {
-    const int lim = L - 2 * K + 1;  // M_2K valid for x < lim
-    for (int i = threadIdx.x; i < nrow * lim; i += blockDim.x) {
-      const int r = i / lim, c = i - r * lim;
-      bufB[r * LS + c] = mm2(bufA[r * LS + c], bufA[r * LS + c + K]);
+// Loads are issued kU at a time ahead of the comparison chain (the walk is
+// otherwise one dependent load per sample).
+constexpr int kU = 8;
+template <class Load, class Slot>
+__device__ __forceinline__ void vhgw_walk(int len, int w, Load in, Slot slot) {
+  for (int b0 = 0; b0 < len; b0 += w) {
+    float2 run = make_float2(CUDART_INF_F, -CUDART_INF_F);
+    int i = b0 + w - 1;
+    for (; i - (kU - 1) >= b0; i -= kU) {  // h: suffix within block b
+      float2 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = in(i - u);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        run = mm2(run, v[u]);
+        if (i - u < len) *slot(i - u) = run;
+      }
     }
-    __syncthreads();
-    float2* t = bufA;
-    bufA = bufB;
-    bufB = t;
-    K *= 2;
-  }
-  for (int i = threadIdx.x; i < nrow * nout; i += blockDim.x) {
-    const int r = i / nout, x = i - r * nout;
-    const float2 v = mm2(bufA[r * LS + x], bufA[r * LS + x + w - K]);
-    const size_t o = plane + (size_t)(y0 + r) * W + x0 + x;
-    hmin[o] = v.x;
-    hmax[o] = v.y;
+    for (; i >= b0; --i) {
+      run = mm2(run, in(i));
+      if (i < len) *slot(i) = run;
+    }
+    const int oe = min(b0 + w, len);
+    // o = b0: the window is block b itself, out = h(b0) already in place
+    float2 g = make_float2(CUDART_INF_F, -CUDART_INF_F);
+    int o = b0 + 1;
+    for (; o + kU - 1 < oe; o += kU) {  // g: prefix within block b + 1
+      float2 v[kU], h[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        v[u] = in(o + u + w - 1);
+        h[u] = *slot(o + u);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        g = mm2(g, v[u]);
+        *slot(o + u) = mm2(h[u], g);
+      }
+    }
+    for (; o < oe; ++o) {
+      g = mm2(g, in(o + w - 1));
+      *slot(o) = mm2(*slot(o), g);
+    }
   }
 }
 
-// Columns pass: block (32, 8), a band of 32 columns x TY output rows.
-__global__ void __launch_bounds__(kThreads) k_bounds_cols(const float* __restrict__ hmin,
-                                                           const float* __restrict__ hmax, int H,
-                                                           int W, int rho, int TY,
-                                                           float* __restrict__ amin,
-                                                           float* __restrict__ bmax,
-                                                           float2* __restrict__ blkmm) {
+// shared memory: F (staged footprint, fp32; reused as O after pass V) and Vm
+__host__ __device__ inline int bounds_pitch(int rho) { return (kBT + 2 * rho) | 1; }
+__host__ __device__ inline size_t bounds_f_bytes(int rho) {
+  const size_t f = sizeof(float) * (size_t)(kBT + 2 * rho) * (kBT + 2 * rho);
+  const size_t o = sizeof(float2) * (size_t)kBT * (kBT + 1);
+  return ((f > o ? f : o) + 15) & ~(size_t)15;
+}
+__host__ inline size_t bounds_smem(int rho, bool stage) {
+  const size_t o = sizeof(float2) * (size_t)kBT * (kBT + 1);
+  return (stage ? bounds_f_bytes(rho) : o) + sizeof(float2) * (size_t)kBT * bounds_pitch(rho);
+}
+
+template <bool kStage>
+__global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ img, int H, int W,
+                                                      int rho, float* __restrict__ amin,
+                                                      float* __restrict__ bmax,
+                                                      float2* __restrict__ blkmm) {
+  extern __shared__ __align__(16) unsigned char smb[];
   __shared__ float2 red[kThreads / 32];
-  extern __shared__ float2 sm2[];
   const int w = 2 * rho + 1;
-  const int x0 = blockIdx.x * kColsCX;
-  const int y0 = blockIdx.y * TY;
+  const int P = bounds_pitch(rho);
+  const size_t fbytes = kStage ? bounds_f_bytes(rho) : sizeof(float2) * (size_t)kBT * (kBT + 1);
+  float* F = reinterpret_cast<float*>(smb);                  // [ny + 2 rho][C]
+  float2* O = reinterpret_cast<float2*>(smb);                // [kBT][kBT + 1] (after pass V)
+  float2* Vm = reinterpret_cast<float2*>(smb + fbytes);      // [kBT][P]
+  const int x0 = blockIdx.x * kBT, y0 = blockIdx.y * kBT;
   const size_t plane = (size_t)blockIdx.z * H * W;
-  const int nrow = min(TY, H - y0);
-  const int L = nrow + 2 * rho;
-  const int LS = TY + 2 * rho;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int x = x0 + tx;
-  const bool colok = x < W;
-  float2* bufA = sm2;
-  float2* bufB = sm2 + LS * kColsCX;
-  for (int r = ty; r < L; r += blockDim.y) {
-    const size_t o = plane + (size_t)reflect_index(y0 - rho + r, H) * W + (colok ? x : 0);
-    bufA[r * kColsCX + tx] = make_float2(__ldg(hmin + o), __ldg(hmax + o));
+  const int nx = min(kBT, W - x0), ny = min(kBT, H - y0);
+  const int C = nx + 2 * rho;  // footprint columns
+  const int R = ny + 2 * rho;  // footprint rows
+  const int tid = threadIdx.x;
+  const float* src = img + plane;
+
+  if (kStage) {  // coalesced staging of the footprint, many loads in flight
+    // cp.async (LDGSTS): every element in flight at once, no register round trip
+    constexpr int kCU = (kBT + 2 * kMaxRho + 31) / 32;  // 32-column chunks per row, max
+    const int lane = tid & 31;
+    int xs[kCU];
+#pragma unroll
+    for (int k = 0; k < kCU; ++k) xs[k] = reflect_index(min(x0 - rho + lane + 32 * k, W - 1 + rho), W);
+    for (int r = tid / 32; r < R; r += kThreads / 32) {
+      const float* rowp = src + (size_t)reflect_index(y0 - rho + r, H) * W;
+#pragma unroll
+      for (int k = 0; k < kCU; ++k)
+        if (lane + 32 * k < C) {
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(F + r * C + lane + 32 * k);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(rowp + xs[k]) : "memory");
+        }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
+  // pass V
+  const int segV = (ny + kBSegV - 1) / kBSegV;
+  for (int t = tid; t < C * segV; t += kThreads) {
+    const int c = t % C, s = t / C;
+    const int o0 = s * kBSegV, len = min(kBSegV, ny - o0);
+    if (kStage) {
+      const float* fc = F + (size_t)o0 * C + c;
+      vhgw_walk(
+          len, w,
+          [&](int i) {
+            const float v = fc[(size_t)i * C];
+            return make_float2(v, v);
+          },
+          [&](int o) { return Vm + (size_t)(o0 + o) * P + c; });
+    } else {
+      const float* col = src + reflect_index(x0 - rho + c, W);
+      const int yb = y0 - rho + o0;
+      vhgw_walk(
+          len, w,
+          [&](int i) {
+            const float v = __ldg(col + (size_t)reflect_index(yb + i, H) * W);
+            return make_float2(v, v);
+          },
+          [&](int o) { return Vm + (size_t)(o0 + o) * P + c; });
+    }
   }
   __syncthreads();
-  int K = 1;
-  while (2 * K <= w) {
-    const int lim = L - 2 * K + 1;
-    for (int r = ty; r < lim; r += blockDim.y)
-      bufB[r * kColsCX + tx] = mm2(bufA[r * kColsCX + tx], bufA[(r + K) * kColsCX + tx]);
-    __syncthreads();
-    float2* t = bufA;
-    bufA = bufB;
-    bufB = t;
-    K *= 2;
+  // pass H (O aliases F, which is dead now)
+  const int segH = (nx + kBSegH - 1) / kBSegH;
+  for (int t = tid; t < ny * segH; t += kThreads) {
+    const int r = t % ny, s = t / ny;
+    const int o0 = s * kBSegH, len = min(kBSegH, nx - o0);
+    const float2* row = Vm + (size_t)r * P + o0;
+    float2* orow = O + (size_t)r * (kBT + 1) + o0;
+    vhgw_walk(
+        len, w, [&](int i) { return row[i]; }, [&](int o) { return orow + o; });
   }
+  __syncthreads();
+  // copy out (coalesced) + the tile's (min alpha, max beta)
   float2 bm = make_float2(CUDART_INF_F, -CUDART_INF_F);
-  if (colok) {
-    for (int r = ty; r < nrow; r += blockDim.y) {
-      const float2 v = mm2(bufA[r * kColsCX + tx], bufA[(r + w - K) * kColsCX + tx]);
-      const size_t o = plane + (size_t)(y0 + r) * W + x;
+  for (int t = tid; t < ny * kBT; t += kThreads) {
+    const int r = t / kBT, x = t % kBT;
+    if (x < nx) {
+      const float2 v = O[(size_t)r * (kBT + 1) + x];
+      const size_t o = plane + (size_t)(y0 + r) * W + x0 + x;
       amin[o] = v.x;
       bmax[o] = v.y;
       bm = mm2(bm, v);
     }
   }
-  if (blkmm) {  // this block's (min alpha, max beta): k_filter's tile centring
-    const int t = ty * kColsCX + tx;
+  if (blkmm) {
     for (int off = 16; off > 0; off >>= 1)
       bm = mm2(bm, make_float2(__shfl_xor_sync(0xffffffffu, bm.x, off),
                                __shfl_xor_sync(0xffffffffu, bm.y, off)));
-    if ((t & 31) == 0) red[t >> 5] = bm;
+    if ((tid & 31) == 0) red[tid >> 5] = bm;
     __syncthreads();
-    if (t == 0) {
+    if (tid == 0) {
       for (int i = 1; i < kThreads / 32; ++i) bm = mm2(bm, red[i]);
       blkmm[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = bm;
     }
@@ -281,7 +344,7 @@ struct FilterArgs {
   const float* beta;
   float* out;
   int B, H, W, rho, TW, SH;
-  const float2* blkmm;  // per (64-row x 32-column) output block: (min alpha, max beta)
+  const float2* blkmm;  // per kBT x kBT bounds tile: (min alpha, max beta)
   unsigned flags;
   float flag_bits;
   int* fb_count;
@@ -376,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     // ---- segment's output blocks (their windows cover the segment footprint)
     float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
     {
-      const int nby = (H + kColsTY - 1) / kColsTY, nbx = (W + kColsCX - 1) / kColsCX;
-      const int by0 = Y0 / kColsTY, by1 = (Y1 - 1) / kColsTY;
-      const int bx0 = x0 / kColsCX, bx1 = min(W - 1, x0 + TW - 1) / kColsCX;
+      const int nby = (H + kBT - 1) / kBT, nbx = (W + kBT - 1) / kBT;
+      const int by0 = Y0 / kBT, by1 = (Y1 - 1) / kBT;
+      const int bx0 = x0 / kBT, bx1 = min(W - 1, x0 + TW - 1) / kBT;
       const int nbw = bx1 - bx0 + 1, nblk = (by1 - by0 + 1) * nbw;
       for (int i = tid; i < nblk; i += kThreads) {
         const int by = by0 + i / nbw, bx = bx0 + i % nbw;
@@ -708,25 +771,24 @@ inline void prof_mark(int i, cudaStream_t st) {
 
 fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta,
                             cudaStream_t st) {
-  const size_t smem_rows = sizeof(float2) * 2 * kRowsRY * (kRowsTX + 2 * kMaxRho);
-  dim3 g1((p->W + kRowsTX - 1) / kRowsTX, (p->H + kRowsRY - 1) / kRowsRY, p->B);
-  prof_mark(0, st);
-  k_bounds_rows<<<g1, kThreads, smem_rows, st>>>(img, p->H, p->W, rho, p->hmin, p->hmax);
-  FABF_CUDA(cudaGetLastError(), "k_bounds_rows launch");
-  prof_mark(1, st);
-  const int TY = kColsTY;
-  const size_t smem_cols = sizeof(float2) * 2 * (TY + 2 * rho) * kColsCX;
+  const bool stage = bounds_smem(rho, true) <= (size_t)kMaxDynSmem;
+  const size_t smem = bounds_smem(rho, stage);
   static bool attr_set = false;
   if (!attr_set) {
-    FABF_CUDA(cudaFuncSetAttribute(k_bounds_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024),
-              "cudaFuncSetAttribute(k_bounds_cols)");
+    FABF_CUDA(cudaFuncSetAttribute(k_bounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+              "cudaFuncSetAttribute(k_bounds)");
+    FABF_CUDA(cudaFuncSetAttribute(k_bounds<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+              "cudaFuncSetAttribute(k_bounds)");
     attr_set = true;
   }
-  dim3 g2((p->W + kColsCX - 1) / kColsCX, (p->H + TY - 1) / TY, p->B);
-  k_bounds_cols<<<g2, dim3(kColsCX, kThreads / kColsCX), smem_cols, st>>>(
-      p->hmin, p->hmax, p->H, p->W, rho, TY, alpha, beta, p->blkmm);
-  FABF_CUDA(cudaGetLastError(), "k_bounds_cols launch");
+  dim3 g((p->W + kBT - 1) / kBT, (p->H + kBT - 1) / kBT, p->B);
+  prof_mark(0, st);
+  if (stage)
+    k_bounds<true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
+  else
+    k_bounds<false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
+  FABF_CUDA(cudaGetLastError(), "k_bounds launch");
+  prof_mark(1, st);
   prof_mark(2, st);
   return FABF_OK;
 }
@@ -883,10 +945,8 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
   cudaError_t e;
   if ((e = cudaMalloc(&p->alpha, px * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&p->beta, px * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&p->hmin, px * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&p->hmax, px * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&p->blkmm, sizeof(float2) * (size_t)batch * ((height + kColsTY - 1) / kColsTY) *
-                                     ((width + kColsCX - 1) / kColsCX))) != cudaSuccess ||
+      (e = cudaMalloc(&p->blkmm, sizeof(float2) * (size_t)batch * ((height + kBT - 1) / kBT) *
+                                     ((width + kBT - 1) / kBT))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_count, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess) {
     fabf_destroy(p);
@@ -983,8 +1043,6 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   if (!p) return FABF_OK;
   cudaFree(p->alpha);
   cudaFree(p->beta);
-  cudaFree(p->hmin);
-  cudaFree(p->hmax);
   cudaFree(p->blkmm);
   cudaFree(p->fb_count);
   cudaFree(p->fb_list);
