@@ -367,7 +367,7 @@ struct FilterSmem {
     off += sizeof(double) * (size_t)NN * L;
     // the pixel queue is double buffered (C2 of step s overlaps A of step s+1)
     qnu = off;
-    off += 2 * sizeof(float) * (size_t)(N + 1) * kThreads;
+    off += 2 * sizeof(double) * (size_t)(N + 1) * kThreads;
     qlam = off;
     off += 2 * sizeof(float) * kThreads;
     qt0 = off;
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   const FilterSmem<N> lay(L, E, w, RB);
   double* Ps = reinterpret_cast<double*>(smraw + lay.ps);  // [RB][N][32*E]
   double* Vs = reinterpret_cast<double*>(smraw + lay.vs);  // [N][L]
-  float* qnu = reinterpret_cast<float*>(smraw + lay.qnu);   // [2][N+1][256]
+  double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [2][N+1][256]
   float* qlam = reinterpret_cast<float*>(smraw + lay.qlam);
   float* qt0 = reinterpret_cast<float*>(smraw + lay.qt0);
   float* qal = reinterpret_cast<float*>(smraw + lay.qal);
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     for (int Yb = Y0; Yb < Y1; Yb += RB, ++step) {
       const int nr = min(RB, Y1 - Yb);
       const int qb = step & 1;
-      float* qnu_b = qnu + (size_t)qb * (N + 1) * kThreads;
+      double* qnu_b = qnu + (size_t)qb * (N + 1) * kThreads;
       float* qlam_b = qlam + qb * kThreads;
       float* qt0_b = qt0 + qb * kThreads;
       float* qal_b = qal + qb * kThreads;
@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // ---- phase C1: stretch + range parameters + enqueue
       {
         int regime = -1;  // -1: no record (invalid, identity or fallback)
-        float nu[N + 1];
+        double nu[N + 1];
         float lam = 0.f, t0 = 0.f;
         if (pvalid) {
           if (p_al == p_be) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
@@ -629,7 +629,12 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               S[q] = row[pos_hi] - (px_x > 0 ? row[pos_lo] : 0.0);
             }
             const double au = ((double)p_al - cT) * invS, bu = ((double)p_be - cT) * invS;
+#ifdef FABF_SKIP_STRETCH  // timing experiment only
+            for (int k = 0; k <= N; ++k) nu[k] = S[k];
+            if (true) {
+#else
             if (nu_from_sums<N>(S, au, bu, nu, a.flag_bits)) {
+#endif
               regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
             } else {  // exact-moment fallback pass writes this pixel
               const int slotfb = atomicAdd(a.fb_count, 1);
@@ -652,8 +657,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
                                           : kThreads - 1 - (baseB + __popc(mB & lt));
 #pragma unroll
           for (int k = 0; k <= N; ++k) qnu_b[k * kThreads + j] = nu[k];
-          qlam_b[j] = lam;
-          qt0_b[j] = t0;
+          qlam_b[j] = p_th;  // theta, sigma: C2 derives lambda, t0 in fp64
+          qt0_b[j] = p_sg;
           qal_b[j] = p_al;
           qbe_b[j] = p_be;
           qo_b[j] = (int)po;
@@ -666,12 +671,19 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       {
         const int j = tid;
         if (j < cntA[qb] || j >= kThreads - cntBC[qb]) {
-          float nu[N + 1];
+          double nu[N + 1];
 #pragma unroll
           for (int k = 0; k <= N; ++k) nu[k] = qnu_b[k * kThreads + j];
           const int o = qo_b[j];
+#ifdef FABF_SKIP_C2  // timing experiment only: no integrals / ratio
+          PixelResult res;
+          res.g = nu[0] + nu[N] + qlam_b[j] + qt0_b[j];
+          res.kappa = res.t2n = 0.f;
+          res.code = 0;
+#else
           PixelResult res = ghat_from_record<N>(nu, qlam_b[j], qt0_b[j], qal_b[j], qbe_b[j],
                                                 qreg_b[j], a.flags, want_t2n, n);
+#endif
           a.out[o] = res.g;
           if (a.d_kappa) a.d_kappa[o] = res.kappa;
           if (a.d_t2n) a.d_t2n[o] = res.t2n;
@@ -712,7 +724,8 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
       if (N >= 1) acc[1] += s;
 #pragma unroll
       for (int k = 1; k < N; ++k) {
-        const double p2 = ((double)(2 * k + 1) * s * p1 - (double)k * p0) / (double)(k + 1);
+        const double p2 = fma((double)(2 * k + 1) / (double)(k + 1) * s, p1,
+                              -((double)k / (double)(k + 1)) * p0);
         acc[k + 1] += p2;
         p0 = p1;
         p1 = p2;
@@ -722,12 +735,13 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
     for (int k = 0; k <= N; ++k)
       for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
     if (lane == 0) {
-      float nu[N + 1];
+      double nu[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) nu[k] = (float)acc[k];
+      for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * acc[k];
       float lam, t0;
-      const int regime = range_params(al, be, a.theta[o], a.sigma[o], lam, t0);
-      PixelResult res = ghat_from_record<N>(nu, lam, t0, al, be, regime, a.flags,
+      const float th = a.theta[o], sg = a.sigma[o];
+      const int regime = range_params(al, be, th, sg, lam, t0);
+      PixelResult res = ghat_from_record<N>(nu, th, sg, al, be, regime, a.flags,
                                             a.d_t2n != nullptr, (float)n);
       a.out[o] = res.g;
       if (a.d_kappa) a.d_kappa[o] = res.kappa;

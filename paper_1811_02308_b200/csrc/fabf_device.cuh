@@ -15,7 +15,10 @@ constexpr int kMaxN = 10;
 constexpr int kGlB = 16;  // fixed-node Gauss-Legendre rule on [0,1], small lambda
 constexpr int kGlC = 24;  // Gauss-Legendre rule on the effective support, far theta_0
 constexpr float kKappaMax = 1000.0f;
-constexpr double kLambdaSmall = 2.0;  // below: fixed-node quadrature (regime B)
+#ifndef FABF_LAMBDA_B
+#define FABF_LAMBDA_B 2.0
+#endif
+constexpr double kLambdaSmall = FABF_LAMBDA_B;  // below: fixed-node quadrature (regime B)
 
 // code bits (mirror FABF_CODE_* in include/fabf.h)
 constexpr unsigned kCodeIdentity = 0x1u;
@@ -35,52 +38,46 @@ __constant__ float c_glB_W[kMaxN + 2][kGlB];
 __constant__ double c_glC_x[kGlC];
 __constant__ double c_glC_w[kGlC];
 
-// Estrin evaluation of sum_{j=LO}^{HI} c[j] x^(j-LO), pw[l] = x^(2^l): the
-// dependency depth is ~log2(terms) instead of Horner's (terms - 1), which is
-// what matters in this latency-bound kernel.
-__host__ __device__ constexpr int estrin_split(int n) {
-  int h = 1;
-  while (2 * h < n) h *= 2;
-  return h;
-}
-__host__ __device__ constexpr int ilog2c(int n) {
-  int l = 0;
-  while ((1 << (l + 1)) <= n) ++l;
-  return l;
-}
-template <int LO, int HI>
-__device__ __forceinline__ double estrin(const double* c, const double* pw) {
-  constexpr int n = HI - LO + 1;
-  if constexpr (n == 1) {
-    return c[LO];
-  } else {
-    constexpr int h = estrin_split(n);
-    return fma(estrin<LO + h, HI>(c, pw), pw[ilog2c(h)], estrin<LO, LO + h - 1>(c, pw));
-  }
-}
+// Horner evaluation of sum_j c[j] x^j with the coefficients in constant
+// memory: every DFMA takes its coefficient as a c[bank][offset] operand (no
+// LDC, no extra registers); the independent seed polynomials of a pixel give
+// the scheduler its ILP.
 template <int DEG>
-__device__ __forceinline__ double poly_estrin(const double* c, double x) {
-  double pw[5];
-  pw[0] = x;
+__device__ __forceinline__ double poly_horner(const double* c, double x) {
+  double p = c[DEG];
 #pragma unroll
-  for (int l = 1; l < 5; ++l) pw[l] = pw[l - 1] * pw[l - 1];
-  return estrin<0, DEG>(c, pw);
+  for (int j = DEG - 1; j >= 0; --j) p = fma(p, x, c[j]);
+  return p;
 }
 
-// exp(z) for z <= 0 in fp64 (z < -708 gives 0): Cody-Waite reduction by ln 2
-// (hi/lo split), degree-12 Taylor polynomial on |r| <= ln2/2 (truncation
-// < 2e-16), 2^k built in the exponent field.  Branch-free; coefficients in
-// constant memory so DFMA reads them as c[] operands.
+// 1/d for normal positive d: MUFU.RCP64H seed + two Newton steps (relative
+// error ~1e-16, no special-case branches: d is in [1, 1e4] here).
+__device__ __forceinline__ double rcp64(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+// exp(z) for z <= 0 in fp64 (z < -708 gives 0): k = rint(z / ln2) by the
+// 1.5 * 2^52 shifter (k lands in the low word, no F2I / FRND), Cody-Waite
+// reduction with a hi/lo ln2, degree-12 Taylor polynomial on |r| <= ln2/2
+// (truncation < 2e-16), 2^k assembled in the exponent field.
 __constant__ double c_exp_poly[13] = {
     1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
     1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600};
 __device__ __forceinline__ double exp_nonpos(double z) {
-  const double kd = rint(z * 1.4426950408889634074);
-  double r = fma(kd, -6.93147180369123816490e-01, z);
+  const double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  const double zc = fmax(z, -708.0);
+  const double ks = fma(zc, 1.4426950408889634074, kShift);
+  const double kd = ks - kShift;
+  double r = fma(kd, -6.93147180369123816490e-01, zc);
   r = fma(kd, -1.90821492927058770002e-10, r);
-  const double p = poly_estrin<12>(c_exp_poly, r);
-  const long long k = (long long)kd;
-  const double scale = __longlong_as_double((k + 1023) << 52);
+  const double p = poly_horner<12>(c_exp_poly, r);
+  const int k = __double2loint(ks);
+  const double scale = __hiloint2double((k + 1023) << 20, 0);
   return (z < -708.0) ? 0.0 : p * scale;
 }
 
@@ -94,73 +91,83 @@ struct PixelResult {
 };
 
 // ---------------------------------------------------------------------------
-// a7: Legendre-Gauss integrals J_k = int_0^1 P~_k(t) exp(-lambda (t-t0)^2) dt,
-// k = 0..N+1, up to one common positive factor per pixel (the ratio eq.(29) and
-// the guard are invariant to it).  P~_k(t) = P_k(2t-1).
+// a7: the integrals of eq.(28) in the Legendre basis.  With s = 2t - 1,
+// kappa = lambda/4, s0 = 2 t0 - 1 and g(s) = exp(-kappa (s - s0)^2):
+//   A_k = int_{-1}^{1} P_k(s) g(s) ds   ( = 2 J_k,  J_k = int_0^1 P~_k psi dt )
+//   X_k = int_{-1}^{1} s P_k(s) g(s) ds = ((k+1) A_{k+1} + k A_{k-1}) / (2k+1)
+// for k = 0..N, up to one common positive factor per pixel (eq.(29) and the
+// guard are invariant to it).  X is what the ratio needs: with the fit
+// p = sum_k (2k+1) nu_k P~_k (a5), T2 = sum_k (2k+1) nu_k A_k and
+// 2 T1 - T2 = sum_k (2k+1) nu_k X_k.
 //
 // Regime A (lambda >= 2, t0 in [-1,2]): the integration-by-parts idea of
-// P:411-426 applied in the Legendre basis.  With s = 2t-1, kappa = lambda/4,
-// s0 = 2t0-1, g(s) = exp(-kappa (s-s0)^2), a_k = int_{-1}^{1} P_k g ds = 2 J_k:
-//   a_{k+1} = [(2k+1)(s0 a_k - (g(1) - (-1)^k g(-1) - D_k)/(2 kappa)) - k a_{k-1}]/(k+1)
-//   D_k     = sum_{j<k, j = k-1 mod 2} (2j+1) a_j
+// P:411-426 applied in the Legendre basis:
+//   X_k     = s0 A_k - (g(1) - (-1)^k g(-1) - D_k) / (2 kappa)
+//   A_{k+1} = ((2k+1) X_k - k A_{k-1}) / (k+1)
+//   D_k     = sum_{j<k, j = k-1 mod 2} (2j+1) A_j
 // (from int P_k g' = [P_k g] - int P_k' g, s P_k = ((k+1)P_{k+1} + k P_{k-1})/(2k+1)
-// and P_k' = sum (2j+1) P_j).  Seeds: a_0 by two erf (eq.(31)) written
-// as erfc = erfcx * exp so that the two boundary exponentials g(+-1) (as in
-// eq.(32)) are reused -- 2 erfcx + 2 exp, branch-free; when t0 is
-// outside [0,1] everything is scaled by exp(kappa (nearer boundary distance)^2).
-// fp64 throughout: the recurrence amplifies seed error ("Kernels").
-// lam and t0 arrive rounded to fp32; kappa is re-derived from the fp32 sqrt so
-// that the seeds and the recurrence describe one and the same problem.
+// and P_k' = sum (2j+1) P_j), so X_k is the recurrence's own intermediate.
+// Seeds: A_0 by two erf (eq.(31)) written as erfc = erfcx * exp so
+// that the two boundary exponentials g(+-1) (as in eq.(32)) are
+// reused -- 2 erfcx + 2 exp, branch-free; when t0 is outside [0,1]
+// everything is scaled by exp(kappa (nearer boundary distance)^2).  fp64
+// throughout: the recurrence amplifies seed error by up to ~4e7 at lambda = 2
+// ("Kernels").  The range parameters come straight from the fp32 inputs in fp64 (their
+// rounding to fp32 would be amplified by kappa up to 1e3):
+//   sk = sqrt(kappa) = (beta-alpha) / (2 sqrt2 sigma), s0 = (2 theta - alpha - beta)/(beta - alpha),
+//   csk = sqrt(pi)/2 / sk, inv2k = 1/(2 kappa).
 template <int N>
-__device__ __forceinline__ void integrals_regime_a(float lam, float t0, float J[N + 2]) {
-  const double sk = (double)sqrtf(0.25f * lam);
-  const double kap = sk * sk;
-  const double s0 = 2.0 * (double)t0 - 1.0;
+__device__ __forceinline__ void integrals_regime_a(double sk, double s0, double csk, double inv2k,
+                                                   double A[N + 1], double X[N + 1]) {
   const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);  // s = +1 and s = -1 ends
   const double qa = xa * xa, qb = xb * xb;
   const bool a_near = qa < qb;
   const double qn = a_near ? qa : qb, qf = a_near ? qb : qa;
   const double E = exp_nonpos(qn - qf);        // <= 1
   const bool inside = (xa >= 0.0) && (xb >= 0.0);
-  const double Gn = inside ? exp_nonpos(-qn) : 1.0;  // scale 1 inside, exp(qn) outside
+  const double Gn = exp_nonpos(inside ? -qn : 0.0);  // scale 1 inside, exp(qn) outside
   const double ca = erfcx_pos(fabs(xa)), cb = erfcx_pos(fabs(xb));
   const double cn = a_near ? ca : cb, cf = a_near ? cb : ca;
   const double gn = Gn, gf = Gn * E;
-  const double c = 0.88622692545275801365 / sk;  // sqrt(pi)/2 / sqrt(kappa)
   // erf(xa) + erf(xb): inside 2 - erfc(xa) - erfc(xb); outside erfc(|x_near|) - erfc(x_far)
-  const double a0 = c * (inside ? (2.0 - cn * gn - cf * gf) : (cn * gn - cf * gf));
+  const double a0 = csk * (inside ? (2.0 - cn * gn - cf * gf) : fma(cn, gn, -cf * gf));
   const double gp = a_near ? gn : gf, gm = a_near ? gf : gn;
-  const double inv2k = 0.5 / kap;  // 1/(2 kappa)
   const double bnd_even = (gp - gm) * inv2k, bnd_odd = (gp + gm) * inv2k;
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
-  J[0] = (float)a0;
+  A[0] = a0;
 #pragma unroll
   for (int k = 0; k <= N; ++k) {
     const double dk = (k & 1) ? d_even : d_odd;
     const double bk = (k & 1) ? bnd_odd : bnd_even;
     const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
-    const double a_next = fma((double)(2 * k + 1) / (double)(k + 1), x,
-                              -((double)k / (double)(k + 1)) * a_prev);
-    if (k & 1)
-      d_odd = fma((double)(2 * k + 1), a_cur, d_odd);
-    else
-      d_even = fma((double)(2 * k + 1), a_cur, d_even);
-    a_prev = a_cur;
-    a_cur = a_next;
-    J[k + 1] = (float)a_next;
+    X[k] = x;
+    if (k < N) {
+      const double a_next = fma((double)(2 * k + 1) / (double)(k + 1), x,
+                                -((double)k / (double)(k + 1)) * a_prev);
+      if (k & 1)
+        d_odd = fma((double)(2 * k + 1), a_cur, d_odd);
+      else
+        d_even = fma((double)(2 * k + 1), a_cur, d_even);
+      a_prev = a_cur;
+      a_cur = a_next;
+      A[k + 1] = a_next;
+    }
   }
 }
 
 // Regime B (lambda < 2, t0 in [-1,2]): the integrand is smooth on [0,1]; a
-// 16-node Gauss-Legendre rule with a constant (N+2) x 16 table, fp32.
+// 16-node Gauss-Legendre rule with a constant (N+2) x 16 table, fp32 (J_k =
+// A_k / 2: one common factor).
 template <int N>
-__device__ __forceinline__ void integrals_regime_b(float lam, float t0, float J[N + 2]) {
+__device__ __forceinline__ void integrals_regime_b(float lam, float t0, float A[N + 1],
+                                                   float X[N + 1]) {
   float E[kGlB];
 #pragma unroll
   for (int q = 0; q < kGlB; ++q) {
     const float z = c_glB_x[q] - t0;
     E[q] = __expf(-lam * z * z);
   }
+  float J[N + 2];
 #pragma unroll
   for (int k = 0; k <= N + 1; ++k) {
     float s = 0.0f;
@@ -168,13 +175,20 @@ __device__ __forceinline__ void integrals_regime_b(float lam, float t0, float J[
     for (int q = 0; q < kGlB; ++q) s = fmaf(c_glB_W[k][q], E[q], s);
     J[k] = s;
   }
+#pragma unroll
+  for (int k = 0; k <= N; ++k) {
+    A[k] = J[k];
+    const float jm = (k > 0) ? (float)k * J[k - 1] : 0.0f;
+    X[k] = fmaf((float)(k + 1), J[k + 1], jm) * (1.0f / (float)(2 * k + 1));
+  }
 }
 
 // Regime C (t0 outside [-1,2]): 24-node Gauss-Legendre on the effective
 // support [a,b] of the integrand (truncated where it has decayed by e^-24 from
 // its value at the nearer end of [0,1]), fp64, scaled by exp(lambda d^2).
 template <int N>
-__device__ __noinline__ void integrals_regime_c(double lam, double t0, float J[N + 2]) {
+__device__ __noinline__ void integrals_regime_c(double lam, double t0, double A[N + 1],
+                                                double X[N + 1]) {
   double a, b, d;
   if (t0 < 0.0) {
     d = -t0;
@@ -196,27 +210,34 @@ __device__ __noinline__ void integrals_regime_c(double lam, double t0, float J[N
     const double s = 2.0 * x - 1.0;
     double p0 = 1.0, p1 = s;
     acc[0] += e;
-    if (N + 1 >= 1) acc[1] += e * s;
+    acc[1] += e * s;
 #pragma unroll
     for (int k = 1; k <= N; ++k) {
-      const double p2 = ((double)(2 * k + 1) * s * p1 - (double)k * p0) / (double)(k + 1);
+      const double p2 = fma((double)(2 * k + 1) / (double)(k + 1) * s, p1,
+                            -((double)k / (double)(k + 1)) * p0);
       acc[k + 1] += e * p2;
       p0 = p1;
       p1 = p2;
     }
   }
 #pragma unroll
-  for (int k = 0; k <= N + 1; ++k) J[k] = (float)acc[k];
+  for (int k = 0; k <= N; ++k) {
+    A[k] = acc[k];
+    const double jm = (k > 0) ? (double)k * acc[k - 1] : 0.0;
+    X[k] = fma((double)(k + 1), acc[k + 1], jm) * (1.0 / (double)(2 * k + 1));
+  }
 }
 
 // ---------------------------------------------------------------------------
-// a6 + a7 + a8: from the Legendre moments nu_k = sum_j P_k(w_j) of the window
-// (w = stretched intensity in [-1,1], eq.(20)-(22)) to g-hat.
-//   T2 = sum_k (2k+1) nu_k J_k  (= sum_k c_k I_k of eq.(29), Legendre form of c = A^{-1} mu)
-//   T1/T2 = 1/2 + 1/2 sum_k nu_k [(k+1) J_{k+1} + k J_{k-1}] / T2
-//   g-hat = alpha + (beta-alpha) T1/T2                     eq.(29)
-// Guard (reading R7): T2 <= 0 or kappa > 1e3 -> the N = 0 value
-// alpha + (beta-alpha) I_1/I_0.
+// a6 + a7 + a8: from the scaled Legendre moments nup_k = (2k+1) sum_j P_k(w_j)
+// of the window (w = stretched intensity in [-1,1], eq.(20)-(22)) to g-hat.
+//   T2 = sum_k nup_k A_k          (= sum_k c_k I_k of eq.(29), Legendre form of c = A^{-1} mu)
+//   U  = sum_k nup_k X_k          (= 2 T1 - T2)
+//   g-hat = alpha + (beta-alpha) T1/T2 = mid + half * U/T2      eq.(29)
+// The sums are fp64 (kappa up to 1e3 multiplies their rounding into the
+// ratio); the ratio itself is rounded to fp32 (its error is 6e-8 * |U/T2|).
+// Guard (reading R7): T2 <= 0 or kappa = sum_k |nup_k A_k| / T2 >
+// 1e3 -> the N = 0 value alpha + (beta-alpha) I_1/I_0, i.e. U/T2 -> X_0/A_0.
 enum Regime : int { kRegA = 0, kRegB = 1, kRegC = 2 };
 
 // a6: lambda = (beta-alpha)^2 / (2 sigma^2) (eq.(25)) and
@@ -224,8 +245,8 @@ enum Regime : int { kRegA = 0, kRegB = 1, kRegC = 2 };
 // output's sensitivity to them is ~1e-5 grey), and the regime.
 __device__ __forceinline__ int range_params(float alpha, float beta, float theta, float sigma,
                                             float& lam, float& t0) {
-  const float d = (float)((double)beta - (double)alpha);
-  t0 = __fdividef((float)((double)theta - (double)alpha), d);
+  const float d = beta - alpha;  // exact unless the range spans >2^24 ulps
+  t0 = __fdividef(theta - alpha, d);
   const float r = __fdividef(d, sigma);
   lam = 0.5f * r * r;
   if (t0 < -1.0f || t0 > 2.0f) return kRegC;
@@ -233,51 +254,74 @@ __device__ __forceinline__ int range_params(float alpha, float beta, float theta
 }
 
 template <int N>
-__device__ __forceinline__ PixelResult ghat_from_record(const float nu[N + 1], float lam, float t0,
-                                                        float alpha, float beta, int regime,
-                                                        unsigned flags, bool want_t2n, float n) {
+__device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1], float theta,
+                                                        float sigma, float alpha, float beta,
+                                                        int regime, unsigned flags, bool want_t2n,
+                                                        float n) {
   PixelResult res;
   res.code = 0u;
-  float J[N + 2];
-  double scale_log = 0.0;  // log of the common factor applied to J (diagnostics only)
-  if (regime == kRegA) {
-    integrals_regime_a<N>(lam, t0, J);
-    if (want_t2n) {
-      const double sk = (double)sqrtf(0.25f * lam), s0 = 2.0 * (double)t0 - 1.0;
-      const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
-      scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
-      scale_log += 0.69314718055994530942;  // a_k = 2 J_k
-    }
-  } else if (regime == kRegB) {
-    integrals_regime_b<N>(lam, t0, J);
-    res.code |= kCodeSmallLambda;
-  } else {
-    integrals_regime_c<N>((double)lam, (double)t0, J);
-    res.code |= kCodeFarTheta;
-    const double dist = t0 < 0.0f ? -(double)t0 : (double)t0 - 1.0;
-    scale_log = (double)lam * dist * dist;
-  }
-  float T2 = 0.0f, U = 0.0f, ab = 0.0f;
+  double scale_log = 0.0;  // log of the common factor applied to A (diagnostics only)
+  float T2f, Uf, abf, A0f, X0f;
+  if (regime == kRegB) {
+    float lam, t0;
+    range_params(alpha, beta, theta, sigma, lam, t0);
+    float A[N + 1], X[N + 1];
+    integrals_regime_b<N>(lam, t0, A, X);
+    float T2 = 0.0f, U = 0.0f, ab = 0.0f;
 #pragma unroll
-  for (int k = 0; k <= N; ++k) {
-    const float t = (float)(2 * k + 1) * nu[k] * J[k];
-    T2 += t;
-    ab += fabsf(t);
-    const float jm = (k > 0) ? (float)k * J[k - 1] : 0.0f;
-    U = fmaf(nu[k], fmaf((float)(k + 1), J[k + 1], jm), U);
+    for (int k = 0; k <= N; ++k) {
+      const float v = (float)nup[k];
+      const float t = v * A[k];
+      T2 += t;
+      ab += fabsf(t);
+      U = fmaf(v, X[k], U);
+    }
+    T2f = T2, Uf = U, abf = ab, A0f = A[0], X0f = X[0];
+    res.code |= kCodeSmallLambda;
+    scale_log = -0.69314718055994530942;  // A = J here
+  } else {
+    double A[N + 1], X[N + 1];
+    const double da = (double)alpha, db = (double)beta, d = db - da, rd = rcp64(d);
+    const double sg = (double)sigma;
+    if (regime == kRegA) {
+      const double s0 = fma(2.0, (double)theta, -(da + db)) * rd;
+      const double sk = 0.35355339059327376220 * d * rcp64(sg);  // d / (2 sqrt2 sigma)
+      const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
+      const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
+      integrals_regime_a<N>(sk, s0, csk, inv2k, A, X);
+      if (want_t2n) {
+        const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
+        scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
+      }
+    } else {
+      const double t0 = ((double)theta - da) * rd;
+      const double r = d / sg, lam = 0.5 * r * r;
+      integrals_regime_c<N>(lam, t0, A, X);
+      res.code |= kCodeFarTheta;
+      const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
+      scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
+    }
+    double T2 = 0.0, U = 0.0, ab = 0.0;
+#pragma unroll
+    for (int k = 0; k <= N; ++k) {
+      T2 = fma(nup[k], A[k], T2);
+      ab = fma(fabs(nup[k]), fabs(A[k]), ab);
+      U = fma(nup[k], X[k], U);
+    }
+    T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A[0], X0f = (float)X[0];
   }
   float ratio;
-  if (!(flags & kFlagLiteral) && (!(T2 > 0.0f) || ab > kKappaMax * T2)) {
-    ratio = J[1] / J[0];
+  if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {
+    ratio = X0f / A0f;
     res.code |= kCodeGuard;
   } else {
-    ratio = U / T2;
+    ratio = Uf / T2f;
   }
-  res.kappa = (T2 > 0.0f) ? ab / T2 : CUDART_INF_F;
-  res.t2n = want_t2n ? (float)((double)T2 / (double)n * exp(-scale_log)) : 0.0f;
-  const double da = (double)alpha, db = (double)beta;
-  const double mid = 0.5 * (da + db), half = 0.5 * (db - da);
-  float g = (float)fma(half, (double)ratio, mid);
+  res.kappa = (T2f > 0.0f) ? abf / T2f : CUDART_INF_F;
+  // T2 / n in the units of eq.(29) (J = A/2, unscaled)
+  res.t2n = want_t2n ? (float)(0.5 * (double)T2f / (double)n * exp(-scale_log)) : 0.0f;
+  const float mid = 0.5f * (alpha + beta), half = 0.5f * (beta - alpha);
+  float g = fmaf(half, ratio, mid);
   if (flags & kFlagClamp) g = fminf(fmaxf(g, alpha), beta);
   res.g = g;
   return res;
@@ -308,7 +352,7 @@ __host__ __device__ constexpr double leg_coef(int k, int r) {
 // Returns false (flag) when the fp64 centring amplification
 // ((1 + |m|)/h)^N exceeds 2^flag_bits ("Numerical envelope").
 template <int N>
-__device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double bu, float nu[N + 1],
+__device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double bu, double nup[N + 1],
                                              float flag_bits) {
   const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
   const float ratio = (float)(1.0 + fabs(m)) / (float)h;
@@ -326,11 +370,11 @@ __device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double 
     p *= ih;
   }
 #pragma unroll
-  for (int k = 0; k <= N; ++k) {
+  for (int k = 0; k <= N; ++k) {  // nup_k = (2k+1) nu_k: the fit's coefficients (a5)
     double v = 0.0;
 #pragma unroll
-    for (int r = k & 1; r <= k; r += 2) v = fma(leg_coef(k, r), S[r], v);
-    nu[k] = (float)v;
+    for (int r = k & 1; r <= k; r += 2) v = fma((double)(2 * k + 1) * leg_coef(k, r), S[r], v);
+    nup[k] = v;
   }
   return true;
 }

@@ -89,9 +89,22 @@ def test_config_full_size_all_pixels(fb, orc, cfg):
     assert np.array_equal(d["alpha"], ra) and np.array_equal(d["beta"], rb)
 
 
-@pytest.mark.parametrize("cfg,scale", [(3, 0.25), (4, 0.12)])
+@pytest.mark.parametrize("cfg,scale", [(3, 0.3), (4, 0.2)])
 def test_config_scaled_all_pixels(fb, orc, cfg, scale):
     w = workloads.config(cfg, scale=scale)
+    out, _, _ = _run(fb, w)
+    o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+    mx, nbad, _ = compare_guarded(out, o, 1.0)
+    assert nbad == 0, f"max |delta| = {mx} grey"
+
+
+@pytest.mark.parametrize("gen,rho,N", [("texture", 2, 10), ("rectangles", 2, 10), ("rectangles", 20, 10),
+                                       ("rectangles", 40, 4), ("texture", 10, 6)])
+def test_config5_cell_all_pixels(fb, orc, gen, rho, N):
+    """Config-5 (rho, N) cells on one 384^2 image of each generator, every pixel.
+    High-kappa pixels here (up to ~900) exposed fp32 rounding of lambda and t0
+    (amplified by kappa), which is why C2 derives them in fp64."""
+    w = workloads.config5(rho, N, batch=1, size=384, generator=gen)
     out, _, _ = _run(fb, w)
     o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
     mx, nbad, _ = compare_guarded(out, o, 1.0)
