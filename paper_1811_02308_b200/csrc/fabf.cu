@@ -50,7 +50,10 @@ constexpr int kThreads = 256;
 #define FABF_FILTER_MINB 2
 #endif
 constexpr int kMaxRho = 96;     // L = TW + 2 rho <= 256 input columns per strip
-constexpr float kFlagBits = 26.0f;
+#ifndef FABF_FLAG_BITS
+#define FABF_FLAG_BITS 32.0f
+#endif
+constexpr float kFlagBits = FABF_FLAG_BITS;
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // opt-in limit minus static shared memory
 
 using Plan = fabf_plan_s;
@@ -324,18 +327,21 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
 }
 
 // ============================================================================
-// steps a2-a8.  Grid (ceil(W/TW), ceil(H/SH), B), 256 threads, RB = 256/TW
-// output rows per step.  Per step:
+// steps a2-a8.  Persistent grid, 256 threads, a CTA walks down vertical
+// segments of strips of TW output columns, RB = 256/TW output rows per step:
 //   A  column owners (thread c < L = TW + 2rho) add the entering row's powers
 //      to / remove the leaving row's powers from their fp64 vertical sums V_q
-//      (kept in shared memory between steps) and write them to Ps;
-//   B  one warp per (row, q): inclusive prefix scan of Ps along the strip
-//      (natural layout, lane l owns entries [lE, lE+E) with E odd: conflict-free);
-//   C1 one pixel per thread: window sums = prefix differences, stretch to
-//      Legendre moments (fp64), range parameters, regime; the record goes to a
+//      (kept in shared memory between steps, odd stride) and write them to Ps;
+//   B  a 16-lane group per (row, q) turns the row into an exclusive prefix
+//      P[0] = 0, P[1 + c] = sum_{c' <= c} V(c') in place (lane l owns E odd
+//      consecutive entries: conflict-free), 4 shuffle rounds;
+//   C1 one pixel per thread: window sums S_q = P[x + w] - P[x], stretch to the
+//      fit's Legendre coefficients (fp64), regime; the record goes to a
 //      shared-memory queue, regime-A records from the front, B/C from the back;
 //   C2 thread j finishes queue record j (integrals, ratio, guard, store), so
 //      warps run one integral regime each except at the A|B boundary.
+constexpr int kSL = 16;  // lanes per prefix scan
+
 struct FilterArgs {
   const float* img;
   const float* theta;
@@ -354,31 +360,36 @@ struct FilterArgs {
   unsigned char* d_code;
 };
 
-template <int N>
+template <int N, int E>
+struct FilterGeom {
+  static constexpr int NN = N > 0 ? N : 1;
+  static constexpr int PSQ = kSL * E + 2;  // one (row, q) prefix row: P[0..16E], even length
+  static constexpr int VST = NN | 1;       // odd per-column stride of the V state
+};
+
+template <int N, int E>
 struct FilterSmem {
   // byte offsets into dynamic shared memory
-  size_t ps, vs, qnu, qlam, qt0, qal, qbe, qo, qreg, total;
-  __host__ __device__ FilterSmem(int L, int E, int w, int RB) {
-    const int NN = N > 0 ? N : 1;
+  size_t ps, vs, qnu, qth, qsg, qal, qbe, qo, total;
+  __host__ __device__ FilterSmem(int L, int RB) {
+    using G = FilterGeom<N, E>;
     size_t off = 0;
     ps = off;
-    off += sizeof(double) * (size_t)RB * NN * 32 * E;
+    off += sizeof(double) * (size_t)RB * G::NN * G::PSQ;
     vs = off;
-    off += sizeof(double) * (size_t)NN * L;
+    off += sizeof(double) * (size_t)G::VST * L;
     // the pixel queue is double buffered (C2 of step s overlaps A of step s+1)
     qnu = off;
     off += 2 * sizeof(double) * (size_t)(N + 1) * kThreads;
-    qlam = off;
+    qth = off;
     off += 2 * sizeof(float) * kThreads;
-    qt0 = off;
+    qsg = off;
     off += 2 * sizeof(float) * kThreads;
     qal = off;
     off += 2 * sizeof(float) * kThreads;
     qbe = off;
     off += 2 * sizeof(float) * kThreads;
     qo = off;
-    off += 2 * sizeof(int) * kThreads;
-    qreg = off;
     off += 2 * sizeof(int) * kThreads;
     total = off;
   }
@@ -389,34 +400,36 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int cntA[2], cntBC[2];
   __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
-  constexpr int NN = N > 0 ? N : 1;
+  using G = FilterGeom<N, E>;
+  constexpr int NN = G::NN, PSQ = G::PSQ, VST = G::VST;
   constexpr int RB = kThreads / TW;  // output rows per step
-  constexpr int PSQ = 32 * E;        // one (row, q) prefix row
   const int rho = a.rho, w = 2 * rho + 1;
   const int H = a.H, W = a.W;
-  const int L = TW + 2 * rho;  // input columns of a strip, <= 32 * E (host picks E)
+  const int L = TW + 2 * rho;  // input columns of a strip, <= 16 * E (host picks E)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const FilterSmem<N> lay(L, E, w, RB);
-  double* Ps = reinterpret_cast<double*>(smraw + lay.ps);  // [RB][N][32*E]
-  double* Vs = reinterpret_cast<double*>(smraw + lay.vs);  // [N][L]
+  const FilterSmem<N, E> lay(L, RB);
+  double* Ps = reinterpret_cast<double*>(smraw + lay.ps);    // [RB][NN][PSQ]
+  double* Vs = reinterpret_cast<double*>(smraw + lay.vs);    // [L][VST]
   double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [2][N+1][256]
-  float* qlam = reinterpret_cast<float*>(smraw + lay.qlam);
-  float* qt0 = reinterpret_cast<float*>(smraw + lay.qt0);
+  float* qth = reinterpret_cast<float*>(smraw + lay.qth);
+  float* qsg = reinterpret_cast<float*>(smraw + lay.qsg);
   float* qal = reinterpret_cast<float*>(smraw + lay.qal);
   float* qbe = reinterpret_cast<float*>(smraw + lay.qbe);
   int* qo = reinterpret_cast<int*>(smraw + lay.qo);
-  int* qreg = reinterpret_cast<int*>(smraw + lay.qreg);
   const float n = (float)(w * w);
   const bool want_t2n = a.d_t2n != nullptr;
+
+  for (int i = tid; i < RB * NN * PSQ; i += kThreads) Ps[i] = 0.0;  // P[0] = 0 for good
 
   // column-owner identity (thread c owns input column c of the strip)
   const int c = tid;
   const bool owner = c < L;
-  const int pos_c = c;  // natural layout; phase B lanes own E (odd) consecutive entries
+  double* vsc = Vs + (owner ? c : 0) * VST;
+  double* psc = Ps + 1 + c;
   // pixel identity within a step
   const int px_r = tid / TW, px_x = tid % TW;
-  const int pos_hi = px_x + 2 * rho;
-  const int pos_lo = px_x > 0 ? px_x - 1 : 0;
+  // phase-B identity
+  const int sgrp = tid / kSL, sl = tid % kSL;
 
   // balanced static schedule: the B * nstrips * H strip-rows are split into
   // gridDim.x contiguous chunks (one per resident CTA); a chunk is one or two
@@ -436,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     const size_t plane = (size_t)bimg * H * W;
 
     // ---- tile-local centre c_T and power-of-two scale s_T: min/max over the
-    // ---- segment's output blocks (their windows cover the segment footprint)
+    // ---- segment's bounds tiles (their windows cover the segment footprint)
     float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
     {
       const int nby = (H + kBT - 1) / kBT, nbx = (W + kBT - 1) / kBT;
@@ -453,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
         lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
       }
+      __syncthreads();  // previous segment's readers of red_* are done
       if (lane == 0) {
         red_min[warp] = lmin;
         red_max[warp] = lmax;
@@ -471,27 +485,27 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     int e2 = 0;
     if (halfr > 0.0) frexp(halfr, &e2);
     const double invS = ldexp(1.0, -e2);  // 1/s_T, s_T = 2^e2 >= half range: exact scaling
+    const double mcs = -cT * invS;         // u = f * invS + mcs, exact
 
-    const int xin = reflect_index(min(x0 - rho + c, W - 1 + rho), W);
-    const float* colp = a.img + plane + xin;  // this thread's input column
+    const float* colp = a.img + plane + reflect_index(min(x0 - rho + c, W - 1 + rho), W);
 
-    // prologue: rows Y0-rho .. Y0+rho-1 (no outputs yet); V starts at zero
+    // prologue: rows Y0-rho-1 .. Y0+rho-1 (the first step removes Y0-rho-1)
     if (owner) {
       double V[NN];
 #pragma unroll
       for (int q = 0; q < NN; ++q) V[q] = 0.0;
-      for (int yin = Y0 - rho; yin < Y0 + rho; ++yin) {
-        const float fv = __ldg(colp + (size_t)reflect_index(yin, H) * W);
-        const double u = ((double)fv - cT) * invS;
-        double pu = u;
+      for (int yin = Y0 - rho - 1; yin < Y0 + rho; ++yin) {
+        const float fv = __ldg(colp + reflect_index(yin, H) * W);
+        const double uu = fma((double)fv, invS, mcs);
+        double pu = uu;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
           V[q] += pu;
-          pu *= u;
+          pu *= uu;
         }
       }
 #pragma unroll
-      for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
+      for (int q = 0; q < N; ++q) vsc[q] = V[q];
     }
 
     // phase-A input prefetch: entering / leaving samples of the next step's rows
@@ -499,28 +513,26 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     auto prefetch = [&](int Yb) {
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const int yin = Yb + r + rho, yout = yin - w;
-        const bool ok = owner && (Yb + r < Y1);
-        pf_in[r] = ok ? __ldg(colp + (size_t)reflect_index(yin, H) * W) : 0.0f;
-        pf_out[r] = (ok && yout >= Y0 - rho) ? __ldg(colp + (size_t)reflect_index(yout, H) * W) : 0.0f;
+        const int yin = min(Yb + r + rho, H - 1 + rho), yout = yin - w;
+        pf_in[r] = __ldg(colp + reflect_index(yin, H) * W);
+        pf_out[r] = __ldg(colp + reflect_index(yout, H) * W);
       }
     };
-    prefetch(Y0);
+    if (owner) prefetch(Y0);
 
     for (int Yb = Y0; Yb < Y1; Yb += RB, ++step) {
       const int nr = min(RB, Y1 - Yb);
       const int qb = step & 1;
       double* qnu_b = qnu + (size_t)qb * (N + 1) * kThreads;
-      float* qlam_b = qlam + qb * kThreads;
-      float* qt0_b = qt0 + qb * kThreads;
+      float* qth_b = qth + qb * kThreads;
+      float* qsg_b = qsg + qb * kThreads;
       float* qal_b = qal + qb * kThreads;
       float* qbe_b = qbe + qb * kThreads;
       int* qo_b = qo + qb * kThreads;
-      int* qreg_b = qreg + qb * kThreads;
       // this thread's pixel parameters (latency hidden behind A and B)
       const int pY = Yb + px_r, pX = x0 + px_x;
       const bool pvalid = (px_r < nr) && (pX < W);
-      const size_t po = plane + (size_t)pY * W + pX;
+      const int po = (int)plane + pY * W + pX;
       float p_al = 0.f, p_be = 0.f, p_th = 0.f, p_sg = 1.f;
       if (pvalid) {
         p_al = __ldg(a.alpha + po);
@@ -543,77 +555,63 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         prefetch(Yb + RB);
         double V[NN];
 #pragma unroll
-        for (int q = 0; q < N; ++q) V[q] = Vs[(size_t)q * L + c];
+        for (int q = 0; q < N; ++q) V[q] = vsc[q];
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
           if (r < nr) {
-            // before the window is full the leaving sample contributes u_o = 0
-            const bool leave = Yb + r - rho - 1 >= Y0 - rho;
-            const double u = ((double)fin[r] - cT) * invS;
-            const double uo = leave ? ((double)fout[r] - cT) * invS : 0.0;
-            double pu = u, po2 = uo;
+            const double ui = fma((double)fin[r], invS, mcs);
+            const double uo = fma((double)fout[r], invS, mcs);
+            double pu = ui, po2 = uo;
 #pragma unroll
             for (int q = 0; q < N; ++q) {
               V[q] += pu - po2;
-              pu *= u;
+              pu *= ui;
               po2 *= uo;
             }
 #pragma unroll
-            for (int q = 0; q < N; ++q) Ps[(r * NN + q) * PSQ + pos_c] = V[q];
+            for (int q = 0; q < N; ++q) psc[(r * NN + q) * PSQ] = V[q];
           }
         }
 #pragma unroll
-        for (int q = 0; q < N; ++q) Vs[(size_t)q * L + c] = V[q];
+        for (int q = 0; q < N; ++q) vsc[q] = V[q];
       }
       __syncthreads();
-      // ---- phase B: inclusive prefix sums over c for each (r, q).  Lane l owns
-      // ---- entries [l*E, l*E+E): with E odd the 8-byte accesses of a warp hit
-      // ---- distinct bank pairs (conflict-free); two scans per warp interleaved.
+      // ---- phase B: exclusive prefix rows, 16 lanes per (r, q)
       if (N > 0) {
-        constexpr int NW = kThreads / 32;
-        for (int s0 = warp; s0 < nr * N; s0 += 2 * NW) {
-          const int s1 = s0 + NW;
-          const bool two = s1 < nr * N;
-          double* row0 = Ps + s0 * PSQ + lane * E;
-          double* row1 = Ps + (two ? s1 : s0) * PSQ + lane * E;
-          double loc0[E], loc1[E];
-          double tot0 = 0.0, tot1 = 0.0;
+        // warp-uniform trip count: both half-warps run the shuffles; a half
+        // without a row of its own re-scans its partner's and does not store
+        for (int b = 2 * warp; b < nr * N; b += kThreads / kSL) {
+          const int s0 = b + (sgrp & 1);
+          const bool act = s0 < nr * N;
+          double* row = Ps + (act ? s0 : b) * PSQ + 1 + sl * E;
+          double loc[E];
+          double tot = 0.0;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            tot0 += row0[e];
-            tot1 += row1[e];
-            loc0[e] = tot0;
-            loc1[e] = tot1;
+            tot += row[e];
+            loc[e] = tot;
           }
-          double inc0 = tot0, inc1 = tot1;
+          double inc = tot;
 #pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const double v0 = __shfl_up_sync(0xffffffffu, inc0, off);
-            const double v1 = __shfl_up_sync(0xffffffffu, inc1, off);
-            if (lane >= off) {
-              inc0 += v0;
-              inc1 += v1;
-            }
+          for (int off = 1; off < kSL; off <<= 1) {
+            const double v = __shfl_up_sync(0xffffffffu, inc, off, kSL);
+            inc += (sl >= off) ? v : 0.0;
           }
-          // exclusive offsets straight from the neighbour (never inc - tot: a
+          // the offset comes straight from the neighbour (never inc - tot: a
           // lane whose chunk runs into the padding carries garbage in tot)
-          double ex0 = __shfl_up_sync(0xffffffffu, inc0, 1);
-          double ex1 = __shfl_up_sync(0xffffffffu, inc1, 1);
-          if (lane == 0) ex0 = ex1 = 0.0;
+          double ex = __shfl_up_sync(0xffffffffu, inc, 1, kSL);
+          ex = (sl == 0) ? 0.0 : ex;
+          if (act) {
 #pragma unroll
-          for (int e = 0; e < E; ++e) row0[e] = loc0[e] + ex0;
-          if (two) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) row1[e] = loc1[e] + ex1;
+            for (int e = 0; e < E; ++e) row[e] = loc[e] + ex;
           }
         }
       }
       __syncthreads();
-      // ---- phase C1: stretch + range parameters + enqueue
+      // ---- phase C1: window sums, stretch, regime, enqueue
       {
         int regime = -1;  // -1: no record (invalid, identity or fallback)
         double nu[N + 1];
-        float lam = 0.f, t0 = 0.f;
         if (pvalid) {
           if (p_al == p_be) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
             a.out[po] = p_al;
@@ -623,22 +621,21 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           } else {
             double S[N + 1];
             S[0] = (double)n;
+            const double* prow = Ps + px_r * NN * PSQ + px_x;
 #pragma unroll
-            for (int q = 1; q <= N; ++q) {
-              const double* row = Ps + (px_r * NN + (q - 1)) * PSQ;
-              S[q] = row[pos_hi] - (px_x > 0 ? row[pos_lo] : 0.0);
-            }
-            const double au = ((double)p_al - cT) * invS, bu = ((double)p_be - cT) * invS;
+            for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
+            const double au = fma((double)p_al, invS, mcs), bu = fma((double)p_be, invS, mcs);
 #ifdef FABF_SKIP_STRETCH  // timing experiment only
             for (int k = 0; k <= N; ++k) nu[k] = S[k];
             if (true) {
 #else
             if (nu_from_sums<N>(S, au, bu, nu, a.flag_bits)) {
 #endif
+              float lam, t0;
               regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
             } else {  // exact-moment fallback pass writes this pixel
               const int slotfb = atomicAdd(a.fb_count, 1);
-              a.fb_list[slotfb] = (int)po;
+              a.fb_list[slotfb] = po;
             }
           }
         }
@@ -657,12 +654,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
                                           : kThreads - 1 - (baseB + __popc(mB & lt));
 #pragma unroll
           for (int k = 0; k <= N; ++k) qnu_b[k * kThreads + j] = nu[k];
-          qlam_b[j] = p_th;  // theta, sigma: C2 derives lambda, t0 in fp64
-          qt0_b[j] = p_sg;
+          qth_b[j] = p_th;
+          qsg_b[j] = p_sg;
           qal_b[j] = p_al;
           qbe_b[j] = p_be;
-          qo_b[j] = (int)po;
-          qreg_b[j] = regime;
+          qo_b[j] = po;
         }
       }
       __syncthreads();
@@ -670,19 +666,25 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // ---- barrier after it: the queue and its counters are double buffered.
       {
         const int j = tid;
-        if (j < cntA[qb] || j >= kThreads - cntBC[qb]) {
+        const int nA = cntA[qb], nBC = cntBC[qb];
+        if (j < nA || j >= kThreads - nBC) {
           double nu[N + 1];
 #pragma unroll
           for (int k = 0; k <= N; ++k) nu[k] = qnu_b[k * kThreads + j];
           const int o = qo_b[j];
+          const float th = qth_b[j], sg = qsg_b[j], al = qal_b[j], be = qbe_b[j];
 #ifdef FABF_SKIP_C2  // timing experiment only: no integrals / ratio
           PixelResult res;
-          res.g = nu[0] + nu[N] + qlam_b[j] + qt0_b[j];
+          res.g = (float)(nu[0] + nu[N]) + th + sg;
           res.kappa = res.t2n = 0.f;
           res.code = 0;
 #else
-          PixelResult res = ghat_from_record<N>(nu, qlam_b[j], qt0_b[j], qal_b[j], qbe_b[j],
-                                                qreg_b[j], a.flags, want_t2n, n);
+          int regime = kRegA;
+          if (j >= nA) {
+            float lam, t0;
+            regime = range_params(al, be, th, sg, lam, t0);
+          }
+          PixelResult res = ghat_from_record<N>(nu, th, sg, al, be, regime, a.flags, want_t2n, n);
 #endif
           a.out[o] = res.g;
           if (a.d_kappa) a.d_kappa[o] = res.kappa;
@@ -809,8 +811,8 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
 
 template <int N, int E, int TW>
 fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
-  const int L = TW + 2 * fa.rho, w = 2 * fa.rho + 1, RB = kThreads / TW;
-  const size_t smem = FilterSmem<N>(L, E, w, RB).total;
+  const int L = TW + 2 * fa.rho, RB = kThreads / TW;
+  const size_t smem = FilterSmem<N, E>(L, RB).total;
   if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
   static int grid_cache[64] = {};  // resident CTAs per device (persistent schedule)
   static size_t smem_cache[64] = {};
@@ -840,15 +842,20 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   (void)B;
   const int L128 = 128 + 2 * fa.rho;
   fabf_status_t s;
-  // prefix rows of 32*E doubles, E odd (conflict-free strided phase-B access)
-  if (L128 <= 160)
-    s = launch_filter_net<N, 5, 128>(fa, st);
-  else if (L128 <= 224)
-    s = launch_filter_net<N, 7, 128>(fa, st);
-  else if (L128 <= 256)
+  // prefix rows of 16*E entries, E odd (conflict-free strided phase-B access)
+  // (column owners: L = TW + 2 rho <= 256 threads)
+  if (L128 <= 16 * 9)
     s = launch_filter_net<N, 9, 128>(fa, st);
+  else if (L128 <= 16 * 11)
+    s = launch_filter_net<N, 11, 128>(fa, st);
+  else if (L128 <= 16 * 13)
+    s = launch_filter_net<N, 13, 128>(fa, st);
+  else if (L128 <= 16 * 15)
+    s = launch_filter_net<N, 15, 128>(fa, st);
+  else if (L128 <= 256)
+    s = launch_filter_net<N, 17, 128>(fa, st);
   else
-    s = launch_filter_net<N, 9, 64>(fa, st);
+    s = launch_filter_net<N, 17, 64>(fa, st);
   if (s != FABF_OK) return s;
   prof_mark(3, st);
   k_fallback<N><<<148 * 2, kThreads, 0, st>>>(fa);

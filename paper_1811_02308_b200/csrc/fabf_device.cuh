@@ -253,6 +253,21 @@ __device__ __forceinline__ int range_params(float alpha, float beta, float theta
   return (lam < (float)kLambdaSmall) ? kRegB : kRegA;
 }
 
+// the fp64 sums of a8 (see above), rounded to fp32 once formed
+template <int N>
+__device__ __forceinline__ void contract(const double nup[N + 1], const double A[N + 1],
+                                         const double X[N + 1], float& T2f, float& Uf, float& abf,
+                                         float& A0f, float& X0f) {
+  double T2 = 0.0, U = 0.0, ab = 0.0;
+#pragma unroll
+  for (int k = 0; k <= N; ++k) {
+    T2 = fma(nup[k], A[k], T2);
+    ab = fma(fabs(nup[k]), fabs(A[k]), ab);
+    U = fma(nup[k], X[k], U);
+  }
+  T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A[0], X0f = (float)X[0];
+}
+
 template <int N>
 __device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1], float theta,
                                                         float sigma, float alpha, float beta,
@@ -279,36 +294,30 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1],
     T2f = T2, Uf = U, abf = ab, A0f = A[0], X0f = X[0];
     res.code |= kCodeSmallLambda;
     scale_log = -0.69314718055994530942;  // A = J here
-  } else {
+  } else if (regime == kRegA) {
     double A[N + 1], X[N + 1];
     const double da = (double)alpha, db = (double)beta, d = db - da, rd = rcp64(d);
     const double sg = (double)sigma;
-    if (regime == kRegA) {
-      const double s0 = fma(2.0, (double)theta, -(da + db)) * rd;
-      const double sk = 0.35355339059327376220 * d * rcp64(sg);  // d / (2 sqrt2 sigma)
-      const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
-      const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
-      integrals_regime_a<N>(sk, s0, csk, inv2k, A, X);
-      if (want_t2n) {
-        const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
-        scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
-      }
-    } else {
-      const double t0 = ((double)theta - da) * rd;
-      const double r = d / sg, lam = 0.5 * r * r;
-      integrals_regime_c<N>(lam, t0, A, X);
-      res.code |= kCodeFarTheta;
-      const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
-      scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
+    const double s0 = fma(2.0, (double)theta, -(da + db)) * rd;
+    const double sk = 0.35355339059327376220 * d * rcp64(sg);  // d / (2 sqrt2 sigma)
+    const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
+    const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
+    integrals_regime_a<N>(sk, s0, csk, inv2k, A, X);
+    if (want_t2n) {
+      const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
+      scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
     }
-    double T2 = 0.0, U = 0.0, ab = 0.0;
-#pragma unroll
-    for (int k = 0; k <= N; ++k) {
-      T2 = fma(nup[k], A[k], T2);
-      ab = fma(fabs(nup[k]), fabs(A[k]), ab);
-      U = fma(nup[k], X[k], U);
-    }
-    T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A[0], X0f = (float)X[0];
+    contract<N>(nup, A, X, T2f, Uf, abf, A0f, X0f);
+  } else {
+    double A[N + 1], X[N + 1];  // (local memory: the regime-C call is out of line)
+    const double da = (double)alpha, db = (double)beta, d = db - da;
+    const double t0 = ((double)theta - da) / d;
+    const double r = d / (double)sigma, lam = 0.5 * r * r;
+    integrals_regime_c<N>(lam, t0, A, X);
+    res.code |= kCodeFarTheta;
+    const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
+    scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
+    contract<N>(nup, A, X, T2f, Uf, abf, A0f, X0f);
   }
   float ratio;
   if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {

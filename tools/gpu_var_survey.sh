@@ -1,7 +1,8 @@
 #!/bin/bash
+# accuracy survey + timing for every variants/*.so
 mkdir -p gpurun_out
-for lib in paper_1811_02308_b200/libfabf.so variants/lamb8.so variants/lamb16.so; do
-  echo "== $lib" >> gpurun_out/survey_L.log
-  FABF_LIB=$PWD/$lib timeout 600 python tools/err_survey.py >> gpurun_out/survey_L.log 2>&1
-  FABF_LIB=$PWD/$lib timeout 300 python tools/time_cfg.py 4 >> gpurun_out/survey_L.log 2>&1
+for lib in variants/*.so; do
+  echo "== $lib" >> gpurun_out/varsurvey_${TAG:-x}.log
+  FABF_LIB=$PWD/$lib timeout 600 python tools/err_survey.py $QUICK >> gpurun_out/varsurvey_${TAG:-x}.log 2>&1
+  for c in ${CFGS:-4 3}; do FABF_LIB=$PWD/$lib timeout 300 python tools/time_cfg.py $c >> gpurun_out/varsurvey_${TAG:-x}.log 2>&1; done
 done
