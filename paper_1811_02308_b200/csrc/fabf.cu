@@ -352,7 +352,7 @@ struct FilterArgs {
   int B, H, W, rho, TW, SH;
   const float2* blkmm;  // per kBT x kBT bounds tile: (min alpha, max beta)
   unsigned flags;
-  float flag_bits;
+  double flag_root;  // 2^(flag_bits / N)
   int* fb_count;
   int* fb_list;
   float* d_kappa;
@@ -514,8 +514,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         const int yin = min(Yb + r + rho, H - 1 + rho), yout = yin - w;
-        pf_in[r] = __ldg(colp + reflect_index(yin, H) * W);
-        pf_out[r] = __ldg(colp + reflect_index(yout, H) * W);
+        pf_in[r] = __ldg(colp + reflect_hi(yin, H) * W);   // yin >= 0
+        pf_out[r] = __ldg(colp + reflect_lo(yout) * W);    // yout < H
       }
     };
     if (owner) prefetch(Y0);
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             for (int k = 0; k <= N; ++k) nu[k] = S[k];
             if (true) {
 #else
-            if (nu_from_sums<N>(S, au, bu, nu, a.flag_bits)) {
+            if (nu_from_sums<N>(S, au, bu, nu, a.flag_root)) {
 #endif
               float lam, t0;
               regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
@@ -927,7 +927,7 @@ fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const f
   fa.SH = 0;  // unused: persistent balanced schedule
   fa.blkmm = p->blkmm;
   fa.flags = p->flags;
-  fa.flag_bits = kFlagBits;
+  fa.flag_root = N > 0 ? std::pow(2.0, (double)kFlagBits / N) : 1e300;
   fa.fb_count = p->fb_count;
   fa.fb_list = p->fb_list;
   fa.d_kappa = diag ? diag->kappa : nullptr;

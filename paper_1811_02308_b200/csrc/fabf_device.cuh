@@ -70,7 +70,7 @@ __constant__ double c_exp_poly[13] = {
     1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600};
 __device__ __forceinline__ double exp_nonpos(double z) {
   const double kShift = 6755399441055744.0;  // 1.5 * 2^52
-  const double zc = fmax(z, -708.0);
+  const double zc = fmax(z, -708.0);  // (z is never NaN here)
   const double ks = fma(zc, 1.4426950408889634074, kShift);
   const double kd = ks - kShift;
   double r = fma(kd, -6.93147180369123816490e-01, zc);
@@ -116,6 +116,12 @@ struct PixelResult {
 // rounding to fp32 would be amplified by kappa up to 1e3):
 //   sk = sqrt(kappa) = (beta-alpha) / (2 sqrt2 sigma), s0 = (2 theta - alpha - beta)/(beta - alpha),
 //   csk = sqrt(pi)/2 / sk, inv2k = 1/(2 kappa).
+// (2k+1)/(k+1) and -k/(k+1), k = 0..kMaxN: c[] operands instead of rebuilt immediates
+__constant__ double c_rec[2 * (kMaxN + 1)] = {
+    1.0, -0.0, 3.0 / 2, -1.0 / 2, 5.0 / 3, -2.0 / 3, 7.0 / 4, -3.0 / 4, 9.0 / 5, -4.0 / 5, 11.0 / 6,
+    -5.0 / 6, 13.0 / 7, -6.0 / 7, 15.0 / 8, -7.0 / 8, 17.0 / 9, -8.0 / 9, 19.0 / 10, -9.0 / 10,
+    21.0 / 11, -10.0 / 11};
+
 template <int N>
 __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double csk, double inv2k,
                                                    double A[N + 1], double X[N + 1]) {
@@ -142,8 +148,7 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
     const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
     X[k] = x;
     if (k < N) {
-      const double a_next = fma((double)(2 * k + 1) / (double)(k + 1), x,
-                                -((double)k / (double)(k + 1)) * a_prev);
+      const double a_next = fma(c_rec[2 * k], x, c_rec[2 * k + 1] * a_prev);
       if (k & 1)
         d_odd = fma((double)(2 * k + 1), a_cur, d_odd);
       else
@@ -359,19 +364,19 @@ __host__ __device__ constexpr double leg_coef(int k, int r) {
 // moments of w = (u - m)/h in [-1,1] (eq.(24) P:341-345 up to the affine map
 // w = 2t - 1); the fixed Legendre table then gives nu_k = sum_j P_k(w_j).
 // Returns false (flag) when the fp64 centring amplification
-// ((1 + |m|)/h)^N exceeds 2^flag_bits ("Numerical envelope").
+// ((1 + |m|)/h)^N exceeds 2^flag_bits ("Numerical envelope"), tested
+// as 1 + |m| > flag_root * h with flag_root = 2^(flag_bits/N) from the host.
 template <int N>
 __device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double bu, double nup[N + 1],
-                                             float flag_bits) {
+                                             double flag_root) {
   const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
-  const float ratio = (float)(1.0 + fabs(m)) / (float)h;
-  if ((float)N * __log2f(ratio) > flag_bits) return false;
+  if (1.0 + fabs(m) > flag_root * h) return false;
 #pragma unroll
   for (int i = 1; i <= N; ++i) {
 #pragma unroll
     for (int k = N; k >= i; --k) S[k] = fma(-m, S[k - 1], S[k]);
   }
-  const double ih = 1.0 / h;
+  const double ih = rcp64(h);
   double p = ih;
 #pragma unroll
   for (int k = 1; k <= N; ++k) {
@@ -388,6 +393,8 @@ __device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double 
   return true;
 }
 
+__device__ __forceinline__ int reflect_hi(int i, int n) { return i < n ? i : 2 * n - 1 - i; }
+__device__ __forceinline__ int reflect_lo(int i) { return i >= 0 ? i : -i - 1; }
 __device__ __forceinline__ int reflect_index(int i, int n) {
   // half-sample symmetric (reading R2); one fold: -n <= i < 2n
   return i < 0 ? -i - 1 : (i >= n ? 2 * n - 1 - i : i);
