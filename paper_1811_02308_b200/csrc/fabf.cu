@@ -158,8 +158,14 @@ fabf_status_t ensure_tables(int dev) {
 // g = prefix op within block b + 1 (running register, empty at o = b w).
 // 3 comparisons per sample and pass whatever rho is; comparisons only: exact.
 constexpr int kBT = 64;    // bounds tile side (output rows and columns)
-constexpr int kBSegV = 32;  // pass-V segment length (rows)
-constexpr int kBSegH = 16;  // pass-H segment length (columns)
+#ifndef FABF_BSEGV
+#define FABF_BSEGV 32
+#endif
+#ifndef FABF_BSEGH
+#define FABF_BSEGH 16
+#endif
+constexpr int kBSegV = FABF_BSEGV;  // pass-V segment length (rows)
+constexpr int kBSegH = FABF_BSEGH;  // pass-H segment length (columns)
 
 __device__ __forceinline__ float2 mm2(float2 a, float2 b) {
   return make_float2(fminf(a.x, b.x), fmaxf(a.y, b.y));
@@ -207,6 +213,64 @@ __device__ __forceinline__ void vhgw_walk(int len, int w, Load in, Slot slot) {
     for (; o < oe; ++o) {
       g = mm2(g, in(o + w - 1));
       *slot(o) = mm2(*slot(o), g);
+    }
+  }
+}
+
+// The same walk over shared memory with 32-bit strides and no per-sample
+// predicates: in[i * sin] (float: min = max = value, or float2), out[o * sout].
+__device__ __forceinline__ float2 mm_in(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 mm_in(float2 v) { return v; }
+template <class TIn>
+__device__ __forceinline__ void vhgw_run(const TIn* __restrict__ in, int sin, float2* __restrict__ out,
+                                         int sout, int len, int w) {
+  constexpr int B8 = 8;  // loads issued in batches ahead of the comparison chain
+  for (int b0 = 0; b0 < len; b0 += w) {
+    float2 run = make_float2(CUDART_INF_F, -CUDART_INF_F);
+    const int top = b0 + w - 1, last = min(top, len - 1);
+    int i = top;
+    for (; i - (B8 - 1) > last; i -= B8) {  // beyond the outputs: no stores
+      TIn v[B8];
+#pragma unroll
+      for (int u = 0; u < B8; ++u) v[u] = in[(i - u) * sin];
+#pragma unroll
+      for (int u = 0; u < B8; ++u) run = mm2(run, mm_in(v[u]));
+    }
+    for (; i > last; --i) run = mm2(run, mm_in(in[i * sin]));
+    for (; i - (B8 - 1) >= b0; i -= B8) {  // h: suffix within block b
+      TIn v[B8];
+#pragma unroll
+      for (int u = 0; u < B8; ++u) v[u] = in[(i - u) * sin];
+#pragma unroll
+      for (int u = 0; u < B8; ++u) {
+        run = mm2(run, mm_in(v[u]));
+        out[(i - u) * sout] = run;
+      }
+    }
+    for (; i >= b0; --i) {
+      run = mm2(run, mm_in(in[i * sin]));
+      out[i * sout] = run;
+    }
+    float2 g = make_float2(CUDART_INF_F, -CUDART_INF_F);
+    const int oe = min(b0 + w, len);
+    int o = b0 + 1;
+    for (; o + (B8 - 1) < oe; o += B8) {  // g: prefix within block b + 1
+      TIn v[B8];
+      float2 h[B8];
+#pragma unroll
+      for (int u = 0; u < B8; ++u) {
+        v[u] = in[(o + u + w - 1) * sin];
+        h[u] = out[(o + u) * sout];
+      }
+#pragma unroll
+      for (int u = 0; u < B8; ++u) {
+        g = mm2(g, mm_in(v[u]));
+        out[(o + u) * sout] = mm2(h[u], g);
+      }
+    }
+    for (; o < oe; ++o) {
+      g = mm2(g, mm_in(in[(o + w - 1) * sin]));
+      out[o * sout] = mm2(out[o * sout], g);
     }
   }
 }
@@ -269,14 +333,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
     const int c = t % C, s = t / C;
     const int o0 = s * kBSegV, len = min(kBSegV, ny - o0);
     if (kStage) {
-      const float* fc = F + (size_t)o0 * C + c;
-      vhgw_walk(
-          len, w,
-          [&](int i) {
-            const float v = fc[(size_t)i * C];
-            return make_float2(v, v);
-          },
-          [&](int o) { return Vm + (size_t)(o0 + o) * P + c; });
+      vhgw_run(F + o0 * C + c, C, Vm + o0 * P + c, P, len, w);
     } else {
       const float* col = src + reflect_index(x0 - rho + c, W);
       const int yb = y0 - rho + o0;
@@ -295,10 +352,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
   for (int t = tid; t < ny * segH; t += kThreads) {
     const int r = t % ny, s = t / ny;
     const int o0 = s * kBSegH, len = min(kBSegH, nx - o0);
-    const float2* row = Vm + (size_t)r * P + o0;
-    float2* orow = O + (size_t)r * (kBT + 1) + o0;
-    vhgw_walk(
-        len, w, [&](int i) { return row[i]; }, [&](int o) { return orow + o; });
+    vhgw_run(Vm + r * P + o0, 1, O + r * (kBT + 1) + o0, 1, len, w);
   }
   __syncthreads();
   // copy out (coalesced) + the tile's (min alpha, max beta)
@@ -371,46 +425,48 @@ template <int N, int E>
 struct FilterSmem {
   // byte offsets into dynamic shared memory
   size_t ps, vs, qnu, qth, qsg, qal, qbe, qo, total;
-  __host__ __device__ FilterSmem(int L, int RB) {
+  __host__ __device__ FilterSmem(int L, int RB, int QS) {
     using G = FilterGeom<N, E>;
     size_t off = 0;
     ps = off;
     off += sizeof(double) * (size_t)RB * G::NN * G::PSQ;
     vs = off;
     off += sizeof(double) * (size_t)G::VST * L;
-    // the pixel queue is double buffered (C2 of step s overlaps A of step s+1)
+    // the pixel queue: C2 of step s reads it before the barrier after A of
+    // step s+1 and C1 of step s+1 writes it after the next one: single buffer
     qnu = off;
-    off += 2 * sizeof(double) * (size_t)(N + 1) * kThreads;
+    off += sizeof(double) * (size_t)(N + 1) * QS;
     qth = off;
-    off += 2 * sizeof(float) * kThreads;
+    off += sizeof(float) * QS;
     qsg = off;
-    off += 2 * sizeof(float) * kThreads;
+    off += sizeof(float) * QS;
     qal = off;
-    off += 2 * sizeof(float) * kThreads;
+    off += sizeof(float) * QS;
     qbe = off;
-    off += 2 * sizeof(float) * kThreads;
+    off += sizeof(float) * QS;
     qo = off;
-    off += 2 * sizeof(int) * kThreads;
+    off += sizeof(int) * QS;
     total = off;
   }
 };
 
-template <int N, int E, int TW>
+template <int N, int E, int TW, int PPT>
 __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int cntA[2], cntBC[2];
   __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
   using G = FilterGeom<N, E>;
   constexpr int NN = G::NN, PSQ = G::PSQ, VST = G::VST;
-  constexpr int RB = kThreads / TW;  // output rows per step
+  constexpr int QS = PPT * kThreads;  // pixels (queue records) per step
+  constexpr int RB = QS / TW;         // output rows per step
   const int rho = a.rho, w = 2 * rho + 1;
   const int H = a.H, W = a.W;
   const int L = TW + 2 * rho;  // input columns of a strip, <= 16 * E (host picks E)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const FilterSmem<N, E> lay(L, RB);
+  const FilterSmem<N, E> lay(L, RB, QS);
   double* Ps = reinterpret_cast<double*>(smraw + lay.ps);    // [RB][NN][PSQ]
   double* Vs = reinterpret_cast<double*>(smraw + lay.vs);    // [L][VST]
-  double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [2][N+1][256]
+  double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [N+1][QS]
   float* qth = reinterpret_cast<float*>(smraw + lay.qth);
   float* qsg = reinterpret_cast<float*>(smraw + lay.qsg);
   float* qal = reinterpret_cast<float*>(smraw + lay.qal);
@@ -426,8 +482,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   const bool owner = c < L;
   double* vsc = Vs + (owner ? c : 0) * VST;
   double* psc = Ps + 1 + c;
-  // pixel identity within a step
-  const int px_r = tid / TW, px_x = tid % TW;
+  // pixel identity within a step: pixels tid + i * kThreads, i < PPT
+  const int px_r = tid / TW, px_x = tid % TW;  // (row px_r + i * kThreads / TW)
   // phase-B identity
   const int sgrp = tid / kSL, sl = tid % kSL;
 
@@ -523,22 +579,24 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     for (int Yb = Y0; Yb < Y1; Yb += RB, ++step) {
       const int nr = min(RB, Y1 - Yb);
       const int qb = step & 1;
-      double* qnu_b = qnu + (size_t)qb * (N + 1) * kThreads;
-      float* qth_b = qth + qb * kThreads;
-      float* qsg_b = qsg + qb * kThreads;
-      float* qal_b = qal + qb * kThreads;
-      float* qbe_b = qbe + qb * kThreads;
-      int* qo_b = qo + qb * kThreads;
       // this thread's pixel parameters (latency hidden behind A and B)
-      const int pY = Yb + px_r, pX = x0 + px_x;
-      const bool pvalid = (px_r < nr) && (pX < W);
-      const int po = (int)plane + pY * W + pX;
-      float p_al = 0.f, p_be = 0.f, p_th = 0.f, p_sg = 1.f;
-      if (pvalid) {
-        p_al = __ldg(a.alpha + po);
-        p_be = __ldg(a.beta + po);
-        p_th = __ldg(a.theta + po);
-        p_sg = __ldg(a.sigma + po);
+      bool pvalid[PPT];
+      int po[PPT];
+      float p_al[PPT], p_be[PPT], p_th[PPT], p_sg[PPT];
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        const int pr = px_r + i * (kThreads / TW);
+        const int pY = Yb + pr, pX = x0 + px_x;
+        pvalid[i] = (pr < nr) && (pX < W);
+        po[i] = (int)plane + pY * W + pX;
+        p_al[i] = p_be[i] = p_th[i] = 0.f;
+        p_sg[i] = 1.f;
+        if (pvalid[i]) {
+          p_al[i] = __ldg(a.alpha + po[i]);
+          p_be[i] = __ldg(a.beta + po[i]);
+          p_th[i] = __ldg(a.theta + po[i]);
+          p_sg[i] = __ldg(a.sigma + po[i]);
+        }
       }
       if (tid == 0) {
         cntA[qb] = 0;
@@ -609,22 +667,23 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       }
       __syncthreads();
       // ---- phase C1: window sums, stretch, regime, enqueue
-      {
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
         int regime = -1;  // -1: no record (invalid, identity or fallback)
         double nu[N + 1];
-        if (pvalid) {
-          if (p_al == p_be) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
-            a.out[po] = p_al;
-            if (a.d_kappa) a.d_kappa[po] = 1.0f;
-            if (a.d_t2n) a.d_t2n[po] = 1.0f;
-            if (a.d_code) a.d_code[po] = (unsigned char)kCodeIdentity;
+        if (pvalid[i]) {
+          if (p_al[i] == p_be[i]) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
+            a.out[po[i]] = p_al[i];
+            if (a.d_kappa) a.d_kappa[po[i]] = 1.0f;
+            if (a.d_t2n) a.d_t2n[po[i]] = 1.0f;
+            if (a.d_code) a.d_code[po[i]] = (unsigned char)kCodeIdentity;
           } else {
             double S[N + 1];
             S[0] = (double)n;
-            const double* prow = Ps + px_r * NN * PSQ + px_x;
+            const double* prow = Ps + (px_r + i * (kThreads / TW)) * NN * PSQ + px_x;
 #pragma unroll
             for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
-            const double au = fma((double)p_al, invS, mcs), bu = fma((double)p_be, invS, mcs);
+            const double au = fma((double)p_al[i], invS, mcs), bu = fma((double)p_be[i], invS, mcs);
 #ifdef FABF_SKIP_STRETCH  // timing experiment only
             for (int k = 0; k <= N; ++k) nu[k] = S[k];
             if (true) {
@@ -632,10 +691,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             if (nu_from_sums<N>(S, au, bu, nu, a.flag_root)) {
 #endif
               float lam, t0;
-              regime = range_params(p_al, p_be, p_th, p_sg, lam, t0);
+              regime = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
             } else {  // exact-moment fallback pass writes this pixel
               const int slotfb = atomicAdd(a.fb_count, 1);
-              a.fb_list[slotfb] = po;
+              a.fb_list[slotfb] = po[i];
             }
           }
         }
@@ -651,45 +710,48 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         const unsigned lt = (1u << lane) - 1u;
         if (regime >= 0) {
           const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
-                                          : kThreads - 1 - (baseB + __popc(mB & lt));
+                                          : QS - 1 - (baseB + __popc(mB & lt));
 #pragma unroll
-          for (int k = 0; k <= N; ++k) qnu_b[k * kThreads + j] = nu[k];
-          qth_b[j] = p_th;
-          qsg_b[j] = p_sg;
-          qal_b[j] = p_al;
-          qbe_b[j] = p_be;
-          qo_b[j] = po;
+          for (int k = 0; k <= N; ++k) qnu[k * QS + j] = nu[k];
+          qth[j] = p_th[i];
+          qsg[j] = p_sg[i];
+          qal[j] = p_al[i];
+          qbe[j] = p_be[i];
+          qo[j] = po[i];
         }
       }
       __syncthreads();
       // ---- phase C2: integrals, ratio, guard, store (one regime per warp).  No
-      // ---- barrier after it: the queue and its counters are double buffered.
+      // ---- barrier after it (see FilterSmem: the counters are double buffered).
       {
-        const int j = tid;
         const int nA = cntA[qb], nBC = cntBC[qb];
-        if (j < nA || j >= kThreads - nBC) {
-          double nu[N + 1];
+#pragma unroll 1
+        for (int i = 0; i < PPT; ++i) {
+          const int j = tid + i * kThreads;
+          if (j < nA || j >= QS - nBC) {
+            double nu[N + 1];
 #pragma unroll
-          for (int k = 0; k <= N; ++k) nu[k] = qnu_b[k * kThreads + j];
-          const int o = qo_b[j];
-          const float th = qth_b[j], sg = qsg_b[j], al = qal_b[j], be = qbe_b[j];
+            for (int k = 0; k <= N; ++k) nu[k] = qnu[k * QS + j];
+            const int o = qo[j];
+            const float th = qth[j], sg = qsg[j], al = qal[j], be = qbe[j];
 #ifdef FABF_SKIP_C2  // timing experiment only: no integrals / ratio
-          PixelResult res;
-          res.g = (float)(nu[0] + nu[N]) + th + sg;
-          res.kappa = res.t2n = 0.f;
-          res.code = 0;
+            PixelResult res;
+            res.g = (float)(nu[0] + nu[N]) + th + sg;
+            res.kappa = res.t2n = 0.f;
+            res.code = 0;
 #else
-          int regime = kRegA;
-          if (j >= nA) {
-            float lam, t0;
-            regime = range_params(al, be, th, sg, lam, t0);
-          }
-          PixelResult res = ghat_from_record<N>(nu, th, sg, al, be, regime, a.flags, want_t2n, n);
+            int regime = kRegA;
+            if (j >= nA) {
+              float lam, t0;
+              regime = range_params(al, be, th, sg, lam, t0);
+            }
+            PixelResult res = ghat_from_record<N>(nu, th, sg, al, be, regime, a.flags, want_t2n, n);
 #endif
-          a.out[o] = res.g;
-          if (a.d_kappa) a.d_kappa[o] = res.kappa;
-          if (a.d_t2n) a.d_t2n[o] = res.t2n;
-          if (a.d_code) a.d_code[o] = (unsigned char)res.code;
+            a.out[o] = res.g;
+            if (a.d_kappa) a.d_kappa[o] = res.kappa;
+            if (a.d_t2n) a.d_t2n[o] = res.t2n;
+            if (a.d_code) a.d_code[o] = (unsigned char)res.code;
+          }
         }
       }
     }
@@ -809,10 +871,14 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
   return FABF_OK;
 }
 
+#ifndef FABF_PPT
+#define FABF_PPT 2
+#endif
 template <int N, int E, int TW>
 fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
-  const int L = TW + 2 * fa.rho, RB = kThreads / TW;
-  const size_t smem = FilterSmem<N, E>(L, RB).total;
+  constexpr int PPT = FABF_PPT;
+  const int L = TW + 2 * fa.rho, QS = PPT * kThreads, RB = QS / TW;
+  const size_t smem = FilterSmem<N, E>(L, RB, QS).total;
   if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
   static int grid_cache[64] = {};  // resident CTAs per device (persistent schedule)
   static size_t smem_cache[64] = {};
@@ -820,11 +886,11 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   if (dev < 0 || dev >= 64) dev = 0;
   if (grid_cache[dev] == 0 || smem_cache[dev] != smem) {
-    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxDynSmem),
               "cudaFuncSetAttribute(k_filter)");
     int per_sm = 0, sms = 0;
-    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW>, kThreads, smem),
+    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT>, kThreads, smem),
               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     FABF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
     grid_cache[dev] = max(1, per_sm) * sms;
@@ -832,7 +898,7 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   }
   const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * fa.H;
   const int grid = (int)std::min<long long>(grid_cache[dev], strips);
-  k_filter<N, E, TW><<<grid, kThreads, smem, st>>>(fa);
+  k_filter<N, E, TW, PPT><<<grid, kThreads, smem, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
   return FABF_OK;
 }

@@ -124,7 +124,8 @@ __constant__ double c_rec[2 * (kMaxN + 1)] = {
 
 template <int N>
 __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double csk, double inv2k,
-                                                   double A[N + 1], double X[N + 1]) {
+                                                   const double nup[N + 1], double& T2, double& U,
+                                                   double& ab, double& A0, double& X0) {
   const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);  // s = +1 and s = -1 ends
   const double qa = xa * xa, qb = xb * xb;
   const bool a_near = qa < qb;
@@ -140,13 +141,19 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
   const double gp = a_near ? gn : gf, gm = a_near ? gf : gn;
   const double bnd_even = (gp - gm) * inv2k, bnd_odd = (gp + gm) * inv2k;
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
-  A[0] = a0;
+  // a8 sums consumed on the fly (no A / X arrays): T2 = sum nup_k A_k,
+  // U = sum nup_k X_k, ab = sum |nup_k A_k|
+  T2 = nup[0] * a0;
+  ab = fabs(T2);
+  U = 0.0;
+  A0 = a0;
 #pragma unroll
   for (int k = 0; k <= N; ++k) {
     const double dk = (k & 1) ? d_even : d_odd;
     const double bk = (k & 1) ? bnd_odd : bnd_even;
     const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
-    X[k] = x;
+    if (k == 0) X0 = x;
+    U = fma(nup[k], x, U);
     if (k < N) {
       const double a_next = fma(c_rec[2 * k], x, c_rec[2 * k + 1] * a_prev);
       if (k & 1)
@@ -155,7 +162,8 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
         d_even = fma((double)(2 * k + 1), a_cur, d_even);
       a_prev = a_cur;
       a_cur = a_next;
-      A[k + 1] = a_next;
+      T2 = fma(nup[k + 1], a_next, T2);
+      ab = fma(fabs(nup[k + 1]), fabs(a_next), ab);
     }
   }
 }
@@ -166,19 +174,15 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
 template <int N>
 __device__ __forceinline__ void integrals_regime_b(float lam, float t0, float A[N + 1],
                                                    float X[N + 1]) {
-  float E[kGlB];
+  float J[N + 2];
+#pragma unroll
+  for (int k = 0; k <= N + 1; ++k) J[k] = 0.0f;
 #pragma unroll
   for (int q = 0; q < kGlB; ++q) {
     const float z = c_glB_x[q] - t0;
-    E[q] = __expf(-lam * z * z);
-  }
-  float J[N + 2];
+    const float e = __expf(-lam * z * z);
 #pragma unroll
-  for (int k = 0; k <= N + 1; ++k) {
-    float s = 0.0f;
-#pragma unroll
-    for (int q = 0; q < kGlB; ++q) s = fmaf(c_glB_W[k][q], E[q], s);
-    J[k] = s;
+    for (int k = 0; k <= N + 1; ++k) J[k] = fmaf(c_glB_W[k][q], e, J[k]);
   }
 #pragma unroll
   for (int k = 0; k <= N; ++k) {
@@ -300,19 +304,19 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1],
     res.code |= kCodeSmallLambda;
     scale_log = -0.69314718055994530942;  // A = J here
   } else if (regime == kRegA) {
-    double A[N + 1], X[N + 1];
     const double da = (double)alpha, db = (double)beta, d = db - da, rd = rcp64(d);
     const double sg = (double)sigma;
     const double s0 = fma(2.0, (double)theta, -(da + db)) * rd;
     const double sk = 0.35355339059327376220 * d * rcp64(sg);  // d / (2 sqrt2 sigma)
     const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
     const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
-    integrals_regime_a<N>(sk, s0, csk, inv2k, A, X);
+    double T2, U, ab, A0, X0;
+    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, T2, U, ab, A0, X0);
+    T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A0, X0f = (float)X0;
     if (want_t2n) {
       const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
       scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
     }
-    contract<N>(nup, A, X, T2f, Uf, abf, A0f, X0f);
   } else {
     double A[N + 1], X[N + 1];  // (local memory: the regime-C call is out of line)
     const double da = (double)alpha, db = (double)beta, d = db - da;
