@@ -221,9 +221,9 @@ __device__ __forceinline__ void vhgw_walk(int len, int w, Load in, Slot slot) {
 // predicates: in[i * sin] (float: min = max = value, or float2), out[o * sout].
 __device__ __forceinline__ float2 mm_in(float v) { return make_float2(v, v); }
 __device__ __forceinline__ float2 mm_in(float2 v) { return v; }
-template <class TIn>
-__device__ __forceinline__ void vhgw_run(const TIn* __restrict__ in, int sin, float2* __restrict__ out,
-                                         int sout, int len, int w) {
+template <class TIn, int sin, int sout>
+__device__ __forceinline__ void vhgw_run(const TIn* __restrict__ in, float2* __restrict__ out, int len,
+                                         int w) {
   constexpr int B8 = 8;  // loads issued in batches ahead of the comparison chain
   for (int b0 = 0; b0 < len; b0 += w) {
     float2 run = make_float2(CUDART_INF_F, -CUDART_INF_F);
@@ -275,31 +275,40 @@ __device__ __forceinline__ void vhgw_run(const TIn* __restrict__ in, int sin, fl
   }
 }
 
-// shared memory: F (staged footprint, fp32; reused as O after pass V) and Vm
-__host__ __device__ inline int bounds_pitch(int rho) { return (kBT + 2 * rho) | 1; }
-__host__ __device__ inline size_t bounds_f_bytes(int rho) {
-  const size_t f = sizeof(float) * (size_t)(kBT + 2 * rho) * (kBT + 2 * rho);
-  const size_t o = sizeof(float2) * (size_t)kBT * (kBT + 1);
+// shared memory: F (staged footprint, fp32, row pitch FP; reused as O after
+// pass V) and Vm (row pitch VP, odd).  Pitches are compile-time per rho class
+// RC (rho <= RC) so that every walk address is a base plus an immediate.
+template <int RC>
+struct BoundsGeom {
+  static constexpr int FP = kBT + 2 * RC;        // >= footprint columns
+  static constexpr int VP = (kBT + 2 * RC) | 1;  // odd: pass-H lanes (rows) conflict-free
+  static constexpr int OP = kBT + 1;
+};
+template <int RC>
+__host__ __device__ inline size_t bounds_f_bytes(int rho, bool stage) {
+  using G = BoundsGeom<RC>;
+  const size_t f = stage ? sizeof(float) * (size_t)(kBT + 2 * rho) * G::FP : 0;
+  const size_t o = sizeof(float2) * (size_t)kBT * G::OP;
   return ((f > o ? f : o) + 15) & ~(size_t)15;
 }
+template <int RC>
 __host__ inline size_t bounds_smem(int rho, bool stage) {
-  const size_t o = sizeof(float2) * (size_t)kBT * (kBT + 1);
-  return (stage ? bounds_f_bytes(rho) : o) + sizeof(float2) * (size_t)kBT * bounds_pitch(rho);
+  return bounds_f_bytes<RC>(rho, stage) + sizeof(float2) * (size_t)kBT * BoundsGeom<RC>::VP;
 }
 
-template <bool kStage>
+template <int RC, bool kStage>
 __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ img, int H, int W,
                                                       int rho, float* __restrict__ amin,
                                                       float* __restrict__ bmax,
                                                       float2* __restrict__ blkmm) {
+  using G = BoundsGeom<RC>;
+  constexpr int FP = G::FP, VP = G::VP, OP = G::OP;
   extern __shared__ __align__(16) unsigned char smb[];
   __shared__ float2 red[kThreads / 32];
   const int w = 2 * rho + 1;
-  const int P = bounds_pitch(rho);
-  const size_t fbytes = kStage ? bounds_f_bytes(rho) : sizeof(float2) * (size_t)kBT * (kBT + 1);
-  float* F = reinterpret_cast<float*>(smb);                  // [ny + 2 rho][C]
-  float2* O = reinterpret_cast<float2*>(smb);                // [kBT][kBT + 1] (after pass V)
-  float2* Vm = reinterpret_cast<float2*>(smb + fbytes);      // [kBT][P]
+  float* F = reinterpret_cast<float*>(smb);                                  // [ny + 2 rho][FP]
+  float2* O = reinterpret_cast<float2*>(smb);                                // [kBT][OP] (after pass V)
+  float2* Vm = reinterpret_cast<float2*>(smb + bounds_f_bytes<RC>(rho, kStage));  // [kBT][VP]
   const int x0 = blockIdx.x * kBT, y0 = blockIdx.y * kBT;
   const size_t plane = (size_t)blockIdx.z * H * W;
   const int nx = min(kBT, W - x0), ny = min(kBT, H - y0);
@@ -310,17 +319,22 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
 
   if (kStage) {  // coalesced staging of the footprint, many loads in flight
     // cp.async (LDGSTS): every element in flight at once, no register round trip
-    constexpr int kCU = (kBT + 2 * kMaxRho + 31) / 32;  // 32-column chunks per row, max
+    constexpr int kCU = (kBT + 2 * RC + 31) / 32;  // 32-column chunks per row, max
     const int lane = tid & 31;
+    const bool interior = x0 - rho >= 0 && x0 + nx + rho <= W && y0 - rho >= 0 && y0 + ny + rho <= H;
     int xs[kCU];
 #pragma unroll
-    for (int k = 0; k < kCU; ++k) xs[k] = reflect_index(min(x0 - rho + lane + 32 * k, W - 1 + rho), W);
+    for (int k = 0; k < kCU; ++k)
+      xs[k] = interior ? x0 - rho + lane + 32 * k
+                       : reflect_index(min(x0 - rho + lane + 32 * k, W - 1 + rho), W);
+    const unsigned fbase = (unsigned)__cvta_generic_to_shared(F);
     for (int r = tid / 32; r < R; r += kThreads / 32) {
-      const float* rowp = src + (size_t)reflect_index(y0 - rho + r, H) * W;
+      const int yr = interior ? y0 - rho + r : reflect_index(y0 - rho + r, H);
+      const float* rowp = src + (size_t)yr * W;
 #pragma unroll
       for (int k = 0; k < kCU; ++k)
         if (lane + 32 * k < C) {
-          const unsigned dst = (unsigned)__cvta_generic_to_shared(F + r * C + lane + 32 * k);
+          const unsigned dst = fbase + 4u * (unsigned)(r * FP + lane + 32 * k);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(rowp + xs[k]) : "memory");
         }
     }
@@ -333,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
     const int c = t % C, s = t / C;
     const int o0 = s * kBSegV, len = min(kBSegV, ny - o0);
     if (kStage) {
-      vhgw_run(F + o0 * C + c, C, Vm + o0 * P + c, P, len, w);
+      vhgw_run<float, FP, VP>(F + o0 * FP + c, Vm + o0 * VP + c, len, w);
     } else {
       const float* col = src + reflect_index(x0 - rho + c, W);
       const int yb = y0 - rho + o0;
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
             const float v = __ldg(col + (size_t)reflect_index(yb + i, H) * W);
             return make_float2(v, v);
           },
-          [&](int o) { return Vm + (size_t)(o0 + o) * P + c; });
+          [&](int o) { return Vm + (size_t)(o0 + o) * VP + c; });
     }
   }
   __syncthreads();
@@ -352,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
   for (int t = tid; t < ny * segH; t += kThreads) {
     const int r = t % ny, s = t / ny;
     const int o0 = s * kBSegH, len = min(kBSegH, nx - o0);
-    vhgw_run(Vm + r * P + o0, 1, O + r * (kBT + 1) + o0, 1, len, w);
+    vhgw_run<float2, 1, 1>(Vm + r * VP + o0, O + r * OP + o0, len, w);
   }
   __syncthreads();
   // copy out (coalesced) + the tile's (min alpha, max beta)
@@ -360,7 +374,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
   for (int t = tid; t < ny * kBT; t += kThreads) {
     const int r = t / kBT, x = t % kBT;
     if (x < nx) {
-      const float2 v = O[(size_t)r * (kBT + 1) + x];
+      const float2 v = O[r * OP + x];
       const size_t o = plane + (size_t)(y0 + r) * W + x0 + x;
       amin[o] = v.x;
       bmax[o] = v.y;
@@ -847,25 +861,43 @@ inline void prof_mark(int i, cudaStream_t st) {
   if (g_prof_ev) cudaEventRecord(g_prof_ev[i], st);
 }
 
-fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta,
-                            cudaStream_t st) {
-  const bool stage = bounds_smem(rho, true) <= (size_t)kMaxDynSmem;
-  const size_t smem = bounds_smem(rho, stage);
+template <int RC>
+fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha, float* beta,
+                               cudaStream_t st) {
+  const bool stage = bounds_smem<RC>(rho, true) <= (size_t)kMaxDynSmem;
+  const size_t smem = bounds_smem<RC>(rho, stage);
   static bool attr_set = false;
   if (!attr_set) {
-    FABF_CUDA(cudaFuncSetAttribute(k_bounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+    FABF_CUDA(cudaFuncSetAttribute(k_bounds<RC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem),
               "cudaFuncSetAttribute(k_bounds)");
-    FABF_CUDA(cudaFuncSetAttribute(k_bounds<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+    FABF_CUDA(cudaFuncSetAttribute(k_bounds<RC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem),
               "cudaFuncSetAttribute(k_bounds)");
     attr_set = true;
   }
   dim3 g((p->W + kBT - 1) / kBT, (p->H + kBT - 1) / kBT, p->B);
-  prof_mark(0, st);
   if (stage)
-    k_bounds<true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
+    k_bounds<RC, true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
   else
-    k_bounds<false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
+    k_bounds<RC, false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
   FABF_CUDA(cudaGetLastError(), "k_bounds launch");
+  return FABF_OK;
+}
+
+fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta,
+                            cudaStream_t st) {
+  prof_mark(0, st);
+  fabf_status_t s;
+  if (rho <= 8)
+    s = launch_bounds_rc<8>(p, img, rho, alpha, beta, st);
+  else if (rho <= 24)
+    s = launch_bounds_rc<24>(p, img, rho, alpha, beta, st);
+  else if (rho <= 48)
+    s = launch_bounds_rc<48>(p, img, rho, alpha, beta, st);
+  else
+    s = launch_bounds_rc<kMaxRho>(p, img, rho, alpha, beta, st);
+  if (s != FABF_OK) return s;
   prof_mark(1, st);
   prof_mark(2, st);
   return FABF_OK;
