@@ -112,18 +112,38 @@ FP64_PEAK_TFLOPS = 64 * 148 * 1.965e9 * 2 / 1e12  # 37.2, derived from unit coun
 
 
 def fp64_flops_per_pixel(N: int) -> int:
-    """Algorithmic fp64 flops per pixel of the dominant kernel (FMA = 2 flops),
+    """Algorithmic fp64 flops per pixel of the dominant kernel k_filter (FMA = 2),
     counted from the method's steps as implemented (DESIGN.md section 4,
-    'Roofline'); halo and prologue recomputation are NOT counted.
-      a3 moments  : entering + leaving sample 2*(2 + (N-1) + N), prefix + difference 2N
-      a4 stretch  : Taylor shift N(N+1)/2 FMA, scaling 2N-1, Legendre sum_k (k//2+1) FMA
-      a7 regime A : 2 erfcx (20 FMA + 2), 2 exp (14 FMA + 1), seeds 10,
-                    recurrence (N+1) * (3 FMA + 1 MUL)
+    'Roofline'); halo columns, prologue rows and the fp32 small-lambda regime
+    are NOT counted (every pixel is charged the regime-A recipe).
+      a3 moments : u of the entering / leaving sample 2*2, powers 2(N-1),
+                   vertical add/sub 2N, prefix add N, window difference N
+      a4 stretch : m, h 4; Taylor shift N(N+1)/2 FMA; scaling 2N-1;
+                   Legendre sum_k (k//2+1) FMA
+      a7 seeds   : range parameters 2 rcp (MUFU + 2 Newton = 4 FMA) + 10;
+                   2 erfcx (rcp 4 FMA, 2 FMA, degree-20 Horner, 1 mul);
+                   2 exp (shifter FMA + add, 2 FMA reduction, degree-12 Horner, 1 mul);
+                   erf combination 8
+      a7 recurrence: per k <= N: X_k 2 FMA, A_{k+1} FMA + mul, D update FMA
+      a8 contraction: per k <= N: 3 FMA (T2, U, |.| sum)
     """
-    a3 = 2 * (2 + (N - 1) + N) + 2 * N
-    a4 = N * (N + 1) + (2 * N - 1) + 2 * sum(k // 2 + 1 for k in range(N + 1))
-    a7 = 2 * (2 * 20 + 2) + 2 * (2 * 14 + 1) + 10 + (N + 1) * (3 * 2 + 1)
-    return a3 + a4 + a7
+    a3 = 2 * 2 + 2 * (N - 1) + 2 * N + N + N
+    a4 = 4 + 2 * (N * (N + 1) // 2) + (2 * N - 1) + 2 * sum(k // 2 + 1 for k in range(N + 1))
+    seeds = 2 * (2 * 4) + 10 + 2 * (2 * 4 + 2 * 2 + 2 * 20 + 1) + 2 * (2 + 1 + 2 * 2 + 2 * 12 + 1) + 8
+    rec = (N + 1) * (2 * 2 + 3 + 2)
+    con = (N + 1) * 3 * 2
+    return a3 + a4 + seeds + rec + con
+
+
+def _traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel`` from
+    the committed ncu --set full capture summary (tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d[kernel]["dram_bytes"]
+    except Exception:
+        return None
 
 
 def _dist():
@@ -138,15 +158,22 @@ def cpu_sample(w, npx: int, seed: int = 0):
     return np.sort(rng.choice(w.img.size, npx, replace=False))
 
 
-def time_oracle(w, npx: int, threads: int | None = None):
+def time_oracle(w, npx: int, threads: int | None = None, seed: int = 0):
     import oracle
 
     oracle.build()
-    idx = cpu_sample(w, npx)
+    idx = cpu_sample(w, npx, seed)
     t = time.perf_counter()
     oracle.fast(w.img, w.theta, w.sigma, w.rho, w.N, pixels=idx, threads=threads)
     dt = time.perf_counter() - t
     return npx / dt / 1e6, dt
+
+
+def oracle_sample_size(w, seconds: float) -> int:
+    """Pixels of a seeded sample the oracle finishes in about ``seconds`` on
+    this host (calibrated on a 2000-pixel sample)."""
+    rate, _ = time_oracle(w, 2000, seed=1)
+    return int(max(2000, min(w.img.size, rate * 1e6 * seconds)))
 
 
 def run_reference(args):
@@ -158,12 +185,14 @@ def run_reference(args):
 
     w = workloads.config(CFG)
     cores = os.cpu_count() or 1
-    npx = args.ref_pixels
-    for _ in range(args.warmup):
-        time_oracle(w, max(64, npx // 10))
+    # each step is a bounded sample sized so the whole run takes a few minutes
+    per_step = max(5.0, min(30.0, args.ref_seconds * 10 / max(1, args.steps + args.warmup)))
+    npx = args.ref_pixels or oracle_sample_size(w, per_step)
+    for i in range(args.warmup):
+        time_oracle(w, max(64, npx // 10), seed=100 + i)
     times = []
-    for _ in range(args.steps):
-        _, dt = time_oracle(w, npx)
+    for i in range(args.steps):
+        _, dt = time_oracle(w, npx, seed=i)
         times.append(dt)
     tot = sum(times)
     value = args.steps * npx / tot / 1e6
@@ -173,6 +202,7 @@ def run_reference(args):
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f128", "data": "synthetic",
         "config": {"workload": w.name, "sample": f"{npx} seeded pixels per step of the 8.29 Mpx frame"},
+        "roofline": None,
         "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
                          "sample": f"{npx} seeded pixels of {w.name} per step"},
         "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -217,29 +247,25 @@ def run_gpu(args):
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if True:
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
+    stage = np.zeros(4)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
+        starts[i].record(stream)
+        # the step itself, with CUDA events between its kernels on the launch
+        # stream (per-kernel device times of the timed region)
+        _, ms4 = fb.filter_profile(plan, img, th, sg, w.rho, w.N, out=out)
+        ends[i].record(stream)
+        stage += np.array(ms4)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    stage /= args.steps
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     tot_ms = float(sum(step_ms))
     fallback = plan.last_fallback_count()
-
-    # per-kernel device times (events recorded between the launches, same stream)
-    stage = np.zeros(4)
-    for i in range(args.steps):
-        flush.fill_(float(i))
-        _, ms4 = fb.filter_profile(plan, img, th, sg, w.rho, w.N, out=out)
-        stage += np.array(ms4)
-    stage /= args.steps
     clk.__exit__(None, None, None)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
@@ -255,12 +281,12 @@ def run_gpu(args):
         fb.filter_host(plan, h_img, h_th, h_sg, w.rho, w.N, h_out)
     e2e_s = time.perf_counter() - t0
 
-    tot = torch.tensor([tot_ms, e2e_s], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
-    tot_ms, e2e_s = float(tot[0]), float(tot[1])
-    value = ws * px * args.steps / (tot_ms * 1e-3) / 1e6
-    e2e_value = ws * px * e2e_steps / e2e_s / 1e6
+    from paper_1811_02308_b200.shard import max_over_ranks, whole_job_rate
+
+    tot_ms = max_over_ranks(tot_ms, dev)  # device time, max over ranks
+    e2e_s = max_over_ranks(e2e_s, dev)
+    value = whole_job_rate(px, args.steps, tot_ms * 1e-3, ws)
+    e2e_value = whole_job_rate(px, e2e_steps, e2e_s, ws)
 
     if rank == 0:
         peaks, peak_src = _load_peaks()
@@ -273,7 +299,8 @@ def run_gpu(args):
         flops = fp64_flops_per_pixel(w.N) * px
         fp64 = {"bound": "alu", "pipe": "fp64", "achieved": flops / (kf_ms * 1e-3) / 1e12,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": flops / (kf_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                "traffic": None, "kernel": "k_filter", "kernel_ms": kf_ms,
+                "traffic": _traffic("k_filter"), "kernel": "k_filter", "kernel_ms": kf_ms,
+                "kernel_share_of_step": kf_ms / ms,
                 "flops_per_pixel": fp64_flops_per_pixel(w.N),
                 "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz x 2 (microbench measured 34.2 TF/s)"}
         line = {
@@ -287,21 +314,69 @@ def run_gpu(args):
             "hbm_roofline": hbm,
             "step_ms": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms)},
             "fallback_pixels": fallback,
-            "stage_ms": {"bounds_rows": stage[0], "bounds_cols": stage[1], "filter": stage[2],
-                         "fallback": stage[3]},
+            "stage_ms": {"k_bounds": stage[0] + stage[1], "k_filter": stage[2], "k_fallback": stage[3]},
             "e2e": {"value": e2e_value, "unit": "Mpix/s", "h2d_bytes_per_step": 12 * px,
                     "d2h_bytes_per_step": 4 * px},
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 3 * args.steps,  # k_bounds, k_filter, k_fallback per step
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            v, dt = time_oracle(w, args.ref_pixels)
+            npx = args.ref_pixels or oracle_sample_size(w, args.ref_seconds)
+            v, dt = time_oracle(w, npx)
             line["cpu_baseline"] = {"value": v, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
-                                    "sample": f"{args.ref_pixels} seeded pixels of {w.name} ({dt:.1f} s)"}
+                                    "sample": f"{npx} seeded pixels of {w.name} ({dt:.1f} s, "
+                                              "__float128 Algorithm 1, all host threads)"}
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_sweep(args):
+    """Config 5: 32 grey 1024^2 images, rho in {2,5,10,20,40} x N in {4,6,8,10},
+    sigma ~ U[5,60], theta = f; one JSON line per (rho, N) cell with Mpix/s and
+    the k_filter fp64 roofline fraction (cost should not depend on rho)."""
+    import torch
+
+    import paper_1811_02308_b200 as fb
+    from paper_1811_02308_b200 import build
+    import workloads
+
+    build.build()
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    gens = [g for g in args.sweep_generators.split(",") if g]
+    for gen in gens:
+        w0 = workloads.config5(2, 4, batch=32, size=1024, generator=gen)
+        img = torch.from_numpy(w0.img).to(dev)
+        th = torch.from_numpy(w0.theta).to(dev)
+        sg = torch.from_numpy(w0.sigma).to(dev)
+        out = torch.empty_like(img)
+        plan = fb.Plan(*w0.shape)
+        px = w0.img.size
+        for rho in (2, 5, 10, 20, 40):
+            for N in (4, 6, 8, 10):
+                for _ in range(max(3, args.warmup)):
+                    fb.filter(plan, img, th, sg, rho, N, out=out)
+                stage = np.zeros(4)
+                for i in range(args.steps):
+                    flush.fill_(float(i))
+                    _, ms4 = fb.filter_profile(plan, img, th, sg, rho, N, out=out)
+                    stage += np.array(ms4)
+                stage /= args.steps
+                ms = float(stage.sum())
+                kf = float(stage[2])
+                fl = fp64_flops_per_pixel(N) * px / (kf * 1e-3) / 1e12
+                print(json.dumps({"sweep": "config5", "generator": gen, "rho": rho, "N": N,
+                                  "images": 32, "size": 1024, "value": px / (ms * 1e-3) / 1e6,
+                                  "unit": "Mpix/s", "ms_per_step": ms,
+                                  "stage_ms": {"k_bounds": stage[0] + stage[1], "k_filter": kf,
+                                               "k_fallback": stage[3]},
+                                  "fallback_pixels": plan.last_fallback_count(),
+                                  "roofline": {"bound": "alu", "pipe": "fp64", "achieved": fl,
+                                               "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                               "frac": fl / FP64_PEAK_TFLOPS}}), flush=True)
     return 0
 
 
@@ -311,11 +386,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fabf", choices=["fabf", "reference"])
-    ap.add_argument("--ref-pixels", type=int, default=20000)
+    ap.add_argument("--ref-pixels", type=int, default=0, help="oracle sample size (0: sized by --ref-seconds)")
+    ap.add_argument("--ref-seconds", type=float, default=15.0, help="target oracle time for cpu_baseline")
+    ap.add_argument("--sweep", action="store_true", help="config-5 (rho, N) sweep, one JSON line per cell")
+    ap.add_argument("--sweep-generators", default="texture,rectangles")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.sweep:
+        return run_sweep(args)
     return run_gpu(args)
 
 
