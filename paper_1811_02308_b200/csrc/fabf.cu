@@ -51,7 +51,7 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kMaxRho = 96;     // L = TW + 2 rho <= 256 input columns per strip
 #ifndef FABF_FLAG_BITS
-#define FABF_FLAG_BITS 32.0f
+#define FABF_FLAG_BITS 40.0f
 #endif
 constexpr float kFlagBits = FABF_FLAG_BITS;
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // opt-in limit minus static shared memory
@@ -464,7 +464,7 @@ struct FilterSmem {
   }
 };
 
-template <int N, int E, int TW, int PPT>
+template <int N, int E, int TW, int PPT, int WD>
 __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int cntA[2], cntBC[2];
@@ -512,7 +512,9 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   for (long long u = u0; u < u1;) {
     const long long seg = u / H;
     const int Y0 = (int)(u - seg * H);
-    const int Y1 = (int)min((long long)H, (long long)Y0 + (u1 - u));
+    // a segment is at most a.SH rows: its centring region (and the error of
+    // its running sums) stays local ("Numerical envelope")
+    const int Y1 = (int)min(min((long long)H, (long long)Y0 + (u1 - u)), (long long)Y0 + a.SH);
     u += Y1 - Y0;
     const int bimg = (int)(seg / nstrips), strip = (int)(seg - (long long)bimg * nstrips);
     const int x0 = strip * TW;
@@ -648,8 +650,9 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         for (int q = 0; q < N; ++q) vsc[q] = V[q];
       }
       __syncthreads();
-      // ---- phase B: exclusive prefix rows, 16 lanes per (r, q)
-      if (N > 0) {
+      // ---- phase B: exclusive prefix rows, 16 lanes per (r, q) (WD > 0: small
+      // ---- windows are summed directly in C1 instead, no prefix magnitudes)
+      if (N > 0 && WD == 0) {
         // warp-uniform trip count: both half-warps run the shuffles; a half
         // without a row of its own re-scans its partner's and does not store
         for (int b = 2 * warp; b < nr * N; b += kThreads / kSL) {
@@ -695,8 +698,18 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             double S[N + 1];
             S[0] = (double)n;
             const double* prow = Ps + (px_r + i * (kThreads / TW)) * NN * PSQ + px_x;
+            if (WD == 0) {
 #pragma unroll
-            for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
+              for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
+            } else {
+#pragma unroll
+              for (int q = 1; q <= N; ++q) {
+                double acc = 0.0;
+#pragma unroll
+                for (int d = 1; d <= WD; ++d) acc += prow[(q - 1) * PSQ + d];
+                S[q] = acc;
+              }
+            }
             const double au = fma((double)p_al[i], invS, mcs), bu = fma((double)p_be[i], invS, mcs);
 #ifdef FABF_SKIP_STRETCH  // timing experiment only
             for (int k = 0; k <= N; ++k) nu[k] = S[k];
@@ -773,14 +786,21 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 }
 
 // ============================================================================
-// exact-moment fallback: one warp per listed pixel; lanes split the window,
-// nu_k = sum_j P_k(w_j) directly in fp64, warp reduction, then the same
-// per-pixel integrals / ratio as k_filter.
-template <int N>
+// exact-moment fallback: nu_k = sum_j P_k(w_j) directly in fp64 over the
+// window of each listed pixel (w_j stretched by the pixel's own alpha, beta:
+// no centring error), then the same per-pixel integrals / ratio as k_filter.
+// kLanes = 1: one thread per pixel (small windows); 32: one warp per pixel,
+// lanes split the window columns.  The Legendre values come from the
+// unnormalised recurrence Q_{k+1} = (2k+1) s Q_k - k^2 Q_{k-1}, Q_k = k! P_k
+// (integer coefficients), divided by k! once at the end.
+__constant__ double c_inv_fact[kMaxN + 1] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120,
+                                             1.0 / 720, 1.0 / 5040, 1.0 / 40320, 1.0 / 362880,
+                                             1.0 / 3628800};
+template <int N, int kLanes>
 __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int sub = (kLanes == 1) ? 0 : (threadIdx.x & 31);
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / kLanes;
+  const int nw = (gridDim.x * blockDim.x) / kLanes;
   const int count = *a.fb_count;
   const int rho = a.rho, w = 2 * rho + 1, n = w * w;
   const int H = a.H, W = a.W;
@@ -793,29 +813,32 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
     double acc[N + 1];
 #pragma unroll
     for (int k = 0; k <= N; ++k) acc[k] = 0.0;
-    for (int j = lane; j < n; j += 32) {
-      const int dy = j / w - rho, dx = j % w - rho;
-      const float fv = img[(size_t)reflect_index(y + dy, H) * W + reflect_index(x + dx, W)];
-      const double s = ((double)fv - mid) * ih;
-      double p0 = 1.0, p1 = s;
-      acc[0] += 1.0;
-      if (N >= 1) acc[1] += s;
+#pragma unroll 4
+    for (int dy = -rho; dy <= rho; ++dy) {  // (unrolled: several rows' loads in flight)
+      const float* row = img + reflect_index(y + dy, H) * W;
+      for (int dx = -rho + sub; dx <= rho; dx += kLanes) {
+        const double sv = ((double)__ldg(row + reflect_index(x + dx, W)) - mid) * ih;
+        double q0 = 1.0, q1 = sv;
+        acc[0] += 1.0;
+        if (N >= 1) acc[1] += sv;
 #pragma unroll
-      for (int k = 1; k < N; ++k) {
-        const double p2 = fma((double)(2 * k + 1) / (double)(k + 1) * s, p1,
-                              -((double)k / (double)(k + 1)) * p0);
-        acc[k + 1] += p2;
-        p0 = p1;
-        p1 = p2;
+        for (int k = 1; k < N; ++k) {
+          const double q2 = fma((double)(2 * k + 1) * q1, sv, -(double)(k * k) * q0);
+          acc[k + 1] += q2;
+          q0 = q1;
+          q1 = q2;
+        }
       }
     }
+    if (kLanes > 1) {
 #pragma unroll
-    for (int k = 0; k <= N; ++k)
-      for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-    if (lane == 0) {
+      for (int k = 0; k <= N; ++k)
+        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+    }
+    if (sub == 0) {
       double nu[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * acc[k];
+      for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * c_inv_fact[k] * acc[k];
       float lam, t0;
       const float th = a.theta[o], sg = a.sigma[o];
       const int regime = range_params(al, be, th, sg, lam, t0);
@@ -906,7 +929,7 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
 #ifndef FABF_PPT
 #define FABF_PPT 2
 #endif
-template <int N, int E, int TW>
+template <int N, int E, int TW, int WD = 0>
 fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   constexpr int PPT = FABF_PPT;
   const int L = TW + 2 * fa.rho, QS = PPT * kThreads, RB = QS / TW;
@@ -918,11 +941,11 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   if (dev < 0 || dev >= 64) dev = 0;
   if (grid_cache[dev] == 0 || smem_cache[dev] != smem) {
-    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT, WD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxDynSmem),
               "cudaFuncSetAttribute(k_filter)");
     int per_sm = 0, sms = 0;
-    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT>, kThreads, smem),
+    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT, WD>, kThreads, smem),
               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     FABF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
     grid_cache[dev] = max(1, per_sm) * sms;
@@ -930,7 +953,7 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   }
   const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * fa.H;
   const int grid = (int)std::min<long long>(grid_cache[dev], strips);
-  k_filter<N, E, TW, PPT><<<grid, kThreads, smem, st>>>(fa);
+  k_filter<N, E, TW, PPT, WD><<<grid, kThreads, smem, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
   return FABF_OK;
 }
@@ -942,7 +965,14 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   fabf_status_t s;
   // prefix rows of 16*E entries, E odd (conflict-free strided phase-B access)
   // (column owners: L = TW + 2 rho <= 256 threads)
-  if (L128 <= 16 * 9)
+  if (fa.rho <= 3) {  // direct window sums (see k_filter, phase B)
+    switch (fa.rho) {
+      case 0: s = launch_filter_net<N, 9, 128, 1>(fa, st); break;
+      case 1: s = launch_filter_net<N, 9, 128, 3>(fa, st); break;
+      case 2: s = launch_filter_net<N, 9, 128, 5>(fa, st); break;
+      default: s = launch_filter_net<N, 9, 128, 7>(fa, st); break;
+    }
+  } else if (L128 <= 16 * 9)
     s = launch_filter_net<N, 9, 128>(fa, st);
   else if (L128 <= 16 * 11)
     s = launch_filter_net<N, 11, 128>(fa, st);
@@ -956,7 +986,8 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
     s = launch_filter_net<N, 17, 64>(fa, st);
   if (s != FABF_OK) return s;
   prof_mark(3, st);
-  k_fallback<N><<<148 * 2, kThreads, 0, st>>>(fa);
+  // one thread per pixel (neighbouring list entries share their windows in L1)
+  k_fallback<N, 1><<<148 * 4, kThreads, 0, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_fallback launch");
   prof_mark(4, st);
   return FABF_OK;
@@ -1022,10 +1053,19 @@ fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const f
   fa.rho = rho;
   fa.B = p->B;
   fa.TW = (rho <= 64) ? 128 : 64;
-  fa.SH = 0;  // unused: persistent balanced schedule
+  // segment cap (rows): fresh fp64 sums every few window heights
+  fa.SH = std::max(64, 3 * (2 * rho + 1));
   fa.blkmm = p->blkmm;
   fa.flags = p->flags;
-  fa.flag_root = N > 0 ? std::pow(2.0, (double)kFlagBits / N) : 1e300;
+  {
+    // fallback flag: amplification ((1+|m|)/h)^N times the magnitude of the
+    // summed terms relative to n (prefix rows: L w / n; direct sums: 1) may
+    // not exceed 2^kFlagBits ("Numerical envelope")
+    const int w = 2 * rho + 1, L = (rho <= 64 ? 128 : 64) + 2 * rho;
+    const double mag = rho <= 3 ? 1.0 : (double)L * w / ((double)w * w);
+    const double bits = (double)kFlagBits - std::log2(mag);
+    fa.flag_root = N > 0 ? std::pow(2.0, bits / N) : 1e300;
+  }
   fa.fb_count = p->fb_count;
   fa.fb_list = p->fb_list;
   fa.d_kappa = diag ? diag->kappa : nullptr;
