@@ -247,23 +247,29 @@ def run_gpu(args):
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    stage = np.zeros(4)
+    # five CUDA events per step around the step's kernels (fabf_filter_events,
+    # recorded on the launch stream, no host sync inside the timed region)
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for evs in kev:
+        for e in evs:
+            e.record(stream)  # creates the handles before the timed region
+    torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
         flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
         starts[i].record(stream)
-        # the step itself, with CUDA events between its kernels on the launch
-        # stream (per-kernel device times of the timed region)
-        _, ms4 = fb.filter_profile(plan, img, th, sg, w.rho, w.N, out=out)
+        fb.filter_events(plan, img, th, sg, w.rho, w.N, kev[i], out=out)
         ends[i].record(stream)
-        stage += np.array(ms4)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    stage /= args.steps
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    stage = np.zeros(4)
+    for evs in kev:
+        stage += np.array([evs[j].elapsed_time(evs[j + 1]) for j in range(4)])
+    stage /= args.steps
     tot_ms = float(sum(step_ms))
     fallback = plan.last_fallback_count()
     clk.__exit__(None, None, None)
@@ -387,7 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fabf", choices=["fabf", "reference"])
     ap.add_argument("--ref-pixels", type=int, default=0, help="oracle sample size (0: sized by --ref-seconds)")
-    ap.add_argument("--ref-seconds", type=float, default=15.0, help="target oracle time for cpu_baseline")
+    ap.add_argument("--ref-seconds", type=float, default=25.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--sweep", action="store_true", help="config-5 (rho, N) sweep, one JSON line per cell")
     ap.add_argument("--sweep-generators", default="texture,rectangles")
     ap.add_argument("--no-cpu-baseline", action="store_true")

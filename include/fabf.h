@@ -116,11 +116,22 @@ fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count);
 
 /* Profiling variant of fabf_filter: same work on the same stream, with CUDA
  * events recorded between the kernels; synchronises the stream and writes the
- * device time (ms) of each stage to stage_ms[0..3] = {bounds rows pass, bounds
- * columns pass, moments + per-pixel filter, exact-moment fallback}.           */
+ * device time (ms) of each stage to stage_ms[0..3] = {bounds (step a1),
+ * always 0 (kept for layout), moments + per-pixel filter (a2-a8), exact-moment
+ * fallback}.                                                                   */
 fabf_status_t fabf_filter_profile(fabf_plan_t plan, const float* img, const float* theta,
                                   const float* sigma, int rho, int N, float* out, void* stream,
                                   float stage_ms[4]);
+
+/* Same work as fabf_filter, recording five caller-owned CUDA events
+ * (cudaEvent_t, created with timing enabled, passed as void*) on `stream`
+ * around the kernels: events[0] before the bounds kernel, [1] and [2] after
+ * it, [3] after the moments + per-pixel kernel, [4] after the fallback kernel.
+ * Does not synchronise: per-kernel device times of a timed region without
+ * perturbing it.  Errors as fabf_filter; NULL events -> INVALID_ARGUMENT.     */
+fabf_status_t fabf_filter_events(fabf_plan_t plan, const float* img, const float* theta,
+                                 const float* sigma, int rho, int N, float* out, void* stream,
+                                 void* const events[5]);
 
 /* Free the plan (NULL is a no-op).  No work using the plan may be pending.   */
 fabf_status_t fabf_destroy(fabf_plan_t plan);

@@ -12,6 +12,7 @@ from .fabf import (  # noqa: F401
     bounds,
     filter,
     filter_diag,
+    filter_events,
     filter_host,
     filter_profile,
     lib,

@@ -1197,6 +1197,22 @@ fabf_status_t fabf_filter_profile(fabf_plan_t plan, const float* img, const floa
   return s;
 }
 
+fabf_status_t fabf_filter_events(fabf_plan_t plan, const float* img, const float* theta,
+                                 const float* sigma, int rho, int N, float* out, void* stream,
+                                 void* const events[5]) {
+  if (!events) return fail(FABF_ERR_INVALID_ARGUMENT, "events is NULL");
+  cudaEvent_t ev[5];
+  for (int i = 0; i < 5; ++i) {
+    if (!events[i]) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL event");
+    ev[i] = (cudaEvent_t)events[i];
+  }
+  g_prof_ev = ev;
+  fabf_status_t s = filter_impl(reinterpret_cast<Plan*>(plan), img, theta, sigma, rho, N, out,
+                                nullptr, (cudaStream_t)stream);
+  g_prof_ev = nullptr;
+  return s;
+}
+
 fabf_status_t fabf_destroy(fabf_plan_t plan) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p) return FABF_OK;

@@ -57,11 +57,12 @@ def lib():
             L.fabf_bounds.argtypes = [P, P, i, P, P, P]
             L.fabf_filter_host.argtypes = [P, P, P, P, i, i, P, P]
             L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
+            L.fabf_filter_events.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_void_p)]
             L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
             L.fabf_destroy.argtypes = [P]
             for fn in ("fabf_plan", "fabf_filter", "fabf_filter_diag", "fabf_bounds",
                        "fabf_filter_host", "fabf_last_fallback_count", "fabf_destroy",
-                       "fabf_filter_profile"):
+                       "fabf_filter_profile", "fabf_filter_events"):
                 getattr(L, fn).restype = ctypes.c_int
             L.fabf_status_string.argtypes = [i]
             L.fabf_status_string.restype = ctypes.c_char_p
@@ -188,6 +189,22 @@ def filter_host(plan: Plan, img, theta, sigma, rho: int, N: int, out, stream=Non
 
     _check(lib().fabf_filter_host(plan.handle, hp(img, "img"), hp(theta, "theta"), hp(sigma, "sigma"),
                                   int(rho), int(N), hp(out, "out"), _stream_ptr(stream)))
+    return out
+
+
+def filter_events(plan: Plan, img, theta, sigma, rho: int, N: int, events, out=None, stream=None):
+    """fabf_filter_events: the step with five caller-owned torch.cuda.Event
+    (timing enabled, already created) recorded around its kernels; no sync."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(img)
+    if len(events) != 5:
+        raise ValueError("five events")
+    arr = (ctypes.c_void_p * 5)(*[ctypes.c_void_p(int(e.cuda_event)) for e in events])
+    _check(lib().fabf_filter_events(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
+                                    _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+                                    _stream_ptr(stream), arr))
     return out
 
 
