@@ -654,40 +654,61 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // ---- windows are summed directly in C1 instead, no prefix magnitudes)
       if (N > 0 && WD == 0) {
         // warp-uniform trip count: both half-warps run the shuffles; a half
-        // without a row of its own re-scans its partner's and does not store
-        for (int b = 2 * warp; b < nr * N; b += kThreads / kSL) {
-          const int s0 = b + (sgrp & 1);
-          const bool act = s0 < nr * N;
-          double* row = Ps + (act ? s0 : b) * PSQ + 1 + sl * E;
-          double loc[E];
-          double tot = 0.0;
+        // without a row of its own re-scans its partner's and does not store.
+        // Two rows per group and pass (s0, s0 + 16): two independent add chains.
+        constexpr int G = kThreads / kSL;  // 16 groups
+        for (int b = 2 * warp; b < nr * N; b += 2 * G) {
+          const int s0 = b + (sgrp & 1), s1 = s0 + G;
+          const bool act0 = s0 < nr * N, act1 = s1 < nr * N;
+          double* row0 = Ps + (act0 ? s0 : b) * PSQ + 1 + sl * E;
+          double* row1 = Ps + (act1 ? s1 : b) * PSQ + 1 + sl * E;
+          double v0[E], v1[E];
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            tot += row[e];
-            loc[e] = tot;
+            v0[e] = row0[e];
+            v1[e] = row1[e];
           }
-          double inc = tot;
+          double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            t0 += v0[e];
+            t1 += v1[e];
+            v0[e] = t0;
+            v1[e] = t1;
+          }
+          double i0 = t0, i1 = t1;
 #pragma unroll
           for (int off = 1; off < kSL; off <<= 1) {
-            const double v = __shfl_up_sync(0xffffffffu, inc, off, kSL);
-            inc += (sl >= off) ? v : 0.0;
+            const double u0 = __shfl_up_sync(0xffffffffu, i0, off, kSL);
+            const double u1 = __shfl_up_sync(0xffffffffu, i1, off, kSL);
+            if (sl >= off) {
+              i0 += u0;
+              i1 += u1;
+            }
           }
           // the offset comes straight from the neighbour (never inc - tot: a
           // lane whose chunk runs into the padding carries garbage in tot)
-          double ex = __shfl_up_sync(0xffffffffu, inc, 1, kSL);
-          ex = (sl == 0) ? 0.0 : ex;
-          if (act) {
+          double e0 = __shfl_up_sync(0xffffffffu, i0, 1, kSL);
+          double e1 = __shfl_up_sync(0xffffffffu, i1, 1, kSL);
+          if (sl == 0) e0 = e1 = 0.0;
+          if (act0) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) row[e] = loc[e] + ex;
+            for (int e = 0; e < E; ++e) row0[e] = v0[e] + e0;
+          }
+          if (act1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) row1[e] = v1[e] + e1;
           }
         }
       }
       __syncthreads();
-      // ---- phase C1: window sums, stretch, regime, enqueue
+      // ---- phase C1: window sums, flag, regime, slot in the queue, stretch
+      // ---- written straight into the slot
 #pragma unroll
       for (int i = 0; i < PPT; ++i) {
         int regime = -1;  // -1: no record (invalid, identity or fallback)
-        double nu[N + 1];
+        double S[N + 1];
+        double au = 0.0, bu = 0.0;
         if (pvalid[i]) {
           if (p_al[i] == p_be[i]) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
             a.out[po[i]] = p_al[i];
@@ -695,33 +716,28 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             if (a.d_t2n) a.d_t2n[po[i]] = 1.0f;
             if (a.d_code) a.d_code[po[i]] = (unsigned char)kCodeIdentity;
           } else {
-            double S[N + 1];
-            S[0] = (double)n;
-            const double* prow = Ps + (px_r + i * (kThreads / TW)) * NN * PSQ + px_x;
-            if (WD == 0) {
-#pragma unroll
-              for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
-            } else {
-#pragma unroll
-              for (int q = 1; q <= N; ++q) {
-                double acc = 0.0;
-#pragma unroll
-                for (int d = 1; d <= WD; ++d) acc += prow[(q - 1) * PSQ + d];
-                S[q] = acc;
-              }
-            }
-            const double au = fma((double)p_al[i], invS, mcs), bu = fma((double)p_be[i], invS, mcs);
-#ifdef FABF_SKIP_STRETCH  // timing experiment only
-            for (int k = 0; k <= N; ++k) nu[k] = S[k];
-            if (true) {
-#else
-            if (nu_from_sums<N>(S, au, bu, nu, a.flag_root)) {
-#endif
-              float lam, t0;
-              regime = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
-            } else {  // exact-moment fallback pass writes this pixel
+            au = fma((double)p_al[i], invS, mcs);
+            bu = fma((double)p_be[i], invS, mcs);
+            if (stretch_flagged(au, bu, a.flag_root)) {  // exact-moment fallback pass
               const int slotfb = atomicAdd(a.fb_count, 1);
               a.fb_list[slotfb] = po[i];
+            } else {
+              float lam, t0;
+              regime = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
+              S[0] = (double)n;
+              const double* prow = Ps + (px_r + i * (kThreads / TW)) * NN * PSQ + px_x;
+              if (WD == 0) {
+#pragma unroll
+                for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
+              } else {
+#pragma unroll
+                for (int q = 1; q <= N; ++q) {
+                  double acc = 0.0;
+#pragma unroll
+                  for (int d = 1; d <= WD; ++d) acc += prow[(q - 1) * PSQ + d];
+                  S[q] = acc;
+                }
+              }
             }
           }
         }
@@ -738,8 +754,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         if (regime >= 0) {
           const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
                                           : QS - 1 - (baseB + __popc(mB & lt));
-#pragma unroll
-          for (int k = 0; k <= N; ++k) qnu[k * QS + j] = nu[k];
+#ifdef FABF_SKIP_STRETCH  // timing experiment only
+          for (int k = 0; k <= N; ++k) qnu[k * QS + j] = S[k];
+#else
+          nu_from_sums<N>(S, au, bu, qnu + j, QS);
+#endif
           qth[j] = p_th[i];
           qsg[j] = p_sg[i];
           qal[j] = p_al[i];
@@ -756,14 +775,12 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         for (int i = 0; i < PPT; ++i) {
           const int j = tid + i * kThreads;
           if (j < nA || j >= QS - nBC) {
-            double nu[N + 1];
-#pragma unroll
-            for (int k = 0; k <= N; ++k) nu[k] = qnu[k * QS + j];
+            const double* nu = qnu + j;  // nu[k * QS]
             const int o = qo[j];
             const float th = qth[j], sg = qsg[j], al = qal[j], be = qbe[j];
 #ifdef FABF_SKIP_C2  // timing experiment only: no integrals / ratio
             PixelResult res;
-            res.g = (float)(nu[0] + nu[N]) + th + sg;
+            res.g = (float)(nu[0] + nu[N * QS]) + th + sg;
             res.kappa = res.t2n = 0.f;
             res.code = 0;
 #else
@@ -772,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               float lam, t0;
               regime = range_params(al, be, th, sg, lam, t0);
             }
-            PixelResult res = ghat_from_record<N>(nu, th, sg, al, be, regime, a.flags, want_t2n, n);
+            PixelResult res = ghat_from_record<N>(nu, QS, th, sg, al, be, regime, a.flags, want_t2n, n);
 #endif
             a.out[o] = res.g;
             if (a.d_kappa) a.d_kappa[o] = res.kappa;
@@ -842,7 +859,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
       float lam, t0;
       const float th = a.theta[o], sg = a.sigma[o];
       const int regime = range_params(al, be, th, sg, lam, t0);
-      PixelResult res = ghat_from_record<N>(nu, th, sg, al, be, regime, a.flags,
+      PixelResult res = ghat_from_record<N>(nu, 1, th, sg, al, be, regime, a.flags,
                                             a.d_t2n != nullptr, (float)n);
       a.out[o] = res.g;
       if (a.d_kappa) a.d_kappa[o] = res.kappa;

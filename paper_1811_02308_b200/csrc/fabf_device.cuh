@@ -124,7 +124,7 @@ __constant__ double c_rec[2 * (kMaxN + 1)] = {
 
 template <int N>
 __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double csk, double inv2k,
-                                                   const double nup[N + 1], double& T2, double& U,
+                                                   const double* nup, int ns, double& T2, double& U,
                                                    double& ab, double& A0, double& X0) {
   const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);  // s = +1 and s = -1 ends
   const double qa = xa * xa, qb = xb * xb;
@@ -143,7 +143,7 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
   // a8 sums consumed on the fly (no A / X arrays): T2 = sum nup_k A_k,
   // U = sum nup_k X_k, ab = sum |nup_k A_k|
-  T2 = nup[0] * a0;
+  T2 = nup[0] * a0;  // (nup[k * ns]: read where used, not held across the seeds)
   ab = fabs(T2);
   U = 0.0;
   A0 = a0;
@@ -153,7 +153,7 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
     const double bk = (k & 1) ? bnd_odd : bnd_even;
     const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
     if (k == 0) X0 = x;
-    U = fma(nup[k], x, U);
+    U = fma(nup[k * ns], x, U);
     if (k < N) {
       const double a_next = fma(c_rec[2 * k], x, c_rec[2 * k + 1] * a_prev);
       if (k & 1)
@@ -162,8 +162,9 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
         d_even = fma((double)(2 * k + 1), a_cur, d_even);
       a_prev = a_cur;
       a_cur = a_next;
-      T2 = fma(nup[k + 1], a_next, T2);
-      ab = fma(fabs(nup[k + 1]), fabs(a_next), ab);
+      const double nk = nup[(k + 1) * ns];
+      T2 = fma(nk, a_next, T2);
+      ab = fma(fabs(nk), fabs(a_next), ab);
     }
   }
 }
@@ -264,21 +265,22 @@ __device__ __forceinline__ int range_params(float alpha, float beta, float theta
 
 // the fp64 sums of a8 (see above), rounded to fp32 once formed
 template <int N>
-__device__ __forceinline__ void contract(const double nup[N + 1], const double A[N + 1],
+__device__ __forceinline__ void contract(const double* nup, int ns, const double A[N + 1],
                                          const double X[N + 1], float& T2f, float& Uf, float& abf,
                                          float& A0f, float& X0f) {
   double T2 = 0.0, U = 0.0, ab = 0.0;
 #pragma unroll
   for (int k = 0; k <= N; ++k) {
-    T2 = fma(nup[k], A[k], T2);
-    ab = fma(fabs(nup[k]), fabs(A[k]), ab);
-    U = fma(nup[k], X[k], U);
+    const double nk = nup[k * ns];
+    T2 = fma(nk, A[k], T2);
+    ab = fma(fabs(nk), fabs(A[k]), ab);
+    U = fma(nk, X[k], U);
   }
   T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A[0], X0f = (float)X[0];
 }
 
 template <int N>
-__device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1], float theta,
+__device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int ns, float theta,
                                                         float sigma, float alpha, float beta,
                                                         int regime, unsigned flags, bool want_t2n,
                                                         float n) {
@@ -294,7 +296,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1],
     float T2 = 0.0f, U = 0.0f, ab = 0.0f;
 #pragma unroll
     for (int k = 0; k <= N; ++k) {
-      const float v = (float)nup[k];
+      const float v = (float)nup[k * ns];
       const float t = v * A[k];
       T2 += t;
       ab += fabsf(t);
@@ -311,7 +313,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1],
     const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
     const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
     double T2, U, ab, A0, X0;
-    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, T2, U, ab, A0, X0);
+    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, ns, T2, U, ab, A0, X0);
     T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A0, X0f = (float)X0;
     if (want_t2n) {
       const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
@@ -326,7 +328,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double nup[N + 1],
     res.code |= kCodeFarTheta;
     const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
     scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
-    contract<N>(nup, A, X, T2f, Uf, abf, A0f, X0f);
+    contract<N>(nup, ns, A, X, T2f, Uf, abf, A0f, X0f);
   }
   float ratio;
   if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {
@@ -370,11 +372,14 @@ __host__ __device__ constexpr double leg_coef(int k, int r) {
 // Returns false (flag) when the fp64 centring amplification
 // ((1 + |m|)/h)^N exceeds 2^flag_bits ("Numerical envelope"), tested
 // as 1 + |m| > flag_root * h with flag_root = 2^(flag_bits/N) from the host.
-template <int N>
-__device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double bu, double nup[N + 1],
-                                             double flag_root) {
+__device__ __forceinline__ bool stretch_flagged(double au, double bu, double flag_root) {
   const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
-  if (1.0 + fabs(m) > flag_root * h) return false;
+  return 1.0 + fabs(m) > flag_root * h;
+}
+template <int N>
+__device__ __forceinline__ void nu_from_sums(double S[N + 1], double au, double bu, double* nup,
+                                             int ns) {
+  const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
 #pragma unroll
   for (int i = 1; i <= N; ++i) {
 #pragma unroll
@@ -392,9 +397,8 @@ __device__ __forceinline__ bool nu_from_sums(double S[N + 1], double au, double 
     double v = 0.0;
 #pragma unroll
     for (int r = k & 1; r <= k; r += 2) v = fma((double)(2 * k + 1) * leg_coef(k, r), S[r], v);
-    nup[k] = v;
+    nup[k * ns] = v;
   }
-  return true;
 }
 
 __device__ __forceinline__ int reflect_hi(int i, int n) { return i < n ? i : 2 * n - 1 - i; }
