@@ -143,6 +143,17 @@ def test_every_degree(fb, orc, N):
     assert nbad == 0, f"N={N}: max |delta| = {mx}"
 
 
+@pytest.mark.parametrize("rho,N", [(10, 9), (10, 10), (20, 10), (40, 6)])
+def test_wide_windows_high_degree(fb, orc, rho, N):
+    """Prefix-row widths E = 11 / 13 with N = 9, 10 run with one pixel per
+    thread per step (shared-memory-driven PPT choice); texture content."""
+    w = workloads.random_case(1, 120, 300, seed=300 + rho + N, kind="texture", rho=rho, N=N)
+    out, _, _ = _run(fb, w)
+    o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+    mx, nbad, _ = compare_guarded(out, o, 1.0)
+    assert nbad == 0, f"rho={rho} N={N}: max |delta| = {mx}"
+
+
 @pytest.mark.parametrize("kind,shape,rho,N", [
     ("rect", (1, 7, 7), 3, 5),          # window == image
     ("rect", (1, 1, 1), 0, 4),          # single pixel
@@ -224,6 +235,25 @@ def test_fallback_path_parity(fb, orc):
     o = orc.fast(f, th, sg, 2, 10)
     mx, nbad, _ = compare_guarded(out, o, 1.0)
     assert nbad == 0, f"max |delta| = {mx}"
+
+
+def test_filter_events_matches_filter(fb):
+    """fabf_filter_events: same output as fabf_filter, five recorded events in
+    kernel order with non-negative gaps (no host sync inside)."""
+    import torch
+
+    w = workloads.config(3, scale=0.25)
+    plan = fb.Plan(*w.shape)
+    img, th, sg = _dev(w.img), _dev(w.theta), _dev(w.sigma)
+    ref = fb.filter(plan, img, th, sg, w.rho, w.N)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    for e in evs:
+        e.record()
+    out = fb.filter_events(plan, img, th, sg, w.rho, w.N, evs)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    gaps = [evs[i].elapsed_time(evs[i + 1]) for i in range(4)]
+    assert all(g >= 0.0 for g in gaps) and gaps[0] > 0.0 and gaps[2] > 0.0
 
 
 def test_host_entry_point_matches_device(fb):
