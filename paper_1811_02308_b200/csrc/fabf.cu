@@ -41,11 +41,17 @@ struct fabf_plan_s {
   float* h_in = nullptr;  // device staging for fabf_filter_host
   float* h_out = nullptr;
   void* last_stream = nullptr;
+  // fabf_filter_host pipeline: copy streams and per-band events
+  static constexpr int kMaxBandsPlan = 8;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t ev_in[kMaxBandsPlan + 1] = {};
+  cudaEvent_t ev_done[kMaxBandsPlan + 1] = {};
 };
 
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMaxBands = fabf_plan_s::kMaxBandsPlan;  // fabf_filter_host row bands
 #ifndef FABF_FILTER_MINB
 #define FABF_FILTER_MINB 2
 #endif
@@ -300,7 +306,7 @@ template <int RC, bool kStage>
 __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ img, int H, int W,
                                                       int rho, float* __restrict__ amin,
                                                       float* __restrict__ bmax,
-                                                      float2* __restrict__ blkmm) {
+                                                      float2* __restrict__ blkmm, int b0, int ty0) {
   using G = BoundsGeom<RC>;
   constexpr int FP = G::FP, VP = G::VP, OP = G::OP;
   extern __shared__ __align__(16) unsigned char smb[];
@@ -309,8 +315,10 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
   float* F = reinterpret_cast<float*>(smb);                                  // [ny + 2 rho][FP]
   float2* O = reinterpret_cast<float2*>(smb);                                // [kBT][OP] (after pass V)
   float2* Vm = reinterpret_cast<float2*>(smb + bounds_f_bytes<RC>(rho, kStage));  // [kBT][VP]
-  const int x0 = blockIdx.x * kBT, y0 = blockIdx.y * kBT;
-  const size_t plane = (size_t)blockIdx.z * H * W;
+  // tile (blockIdx.x, ty0 + blockIdx.y) of image b0 + blockIdx.z (row bands: fabf_filter_host)
+  const int ty = ty0 + blockIdx.y, bimg = b0 + blockIdx.z;
+  const int x0 = blockIdx.x * kBT, y0 = ty * kBT;
+  const size_t plane = (size_t)bimg * H * W;
   const int nx = min(kBT, W - x0), ny = min(kBT, H - y0);
   const int C = nx + 2 * rho;  // footprint columns
   const int R = ny + 2 * rho;  // footprint rows
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
     __syncthreads();
     if (tid == 0) {
       for (int i = 1; i < kThreads / 32; ++i) bm = mm2(bm, red[i]);
-      blkmm[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = bm;
+      blkmm[((size_t)bimg * ((H + kBT - 1) / kBT) + ty) * gridDim.x + blockIdx.x] = bm;
     }
   }
 }
@@ -418,6 +426,7 @@ struct FilterArgs {
   const float* beta;
   float* out;
   int B, H, W, rho, TW, SH;
+  int b0, r0, r1;  // images [b0, b0 + B), rows [r0, r1) of each (row bands)
   const float2* blkmm;  // per kBT x kBT bounds tile: (min alpha, max beta)
   unsigned flags;
   double flag_root;  // 2^(flag_bits / N)
@@ -505,18 +514,20 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   // gridDim.x contiguous chunks (one per resident CTA); a chunk is one or two
   // vertical segments of a strip, each walked top to bottom.
   const int nstrips = (W + TW - 1) / TW;
-  const long long U = (long long)a.B * nstrips * H;
+  const int HR = a.r1 - a.r0;  // rows of the band
+  const long long U = (long long)a.B * nstrips * HR;
   const long long u0 = (long long)blockIdx.x * U / gridDim.x;
   const long long u1 = (long long)(blockIdx.x + 1) * U / gridDim.x;
   int step = 0;
   for (long long u = u0; u < u1;) {
-    const long long seg = u / H;
-    const int Y0 = (int)(u - seg * H);
+    const long long seg = u / HR;
+    const int Y0 = a.r0 + (int)(u - seg * HR);
     // a segment is at most a.SH rows: its centring region (and the error of
     // its running sums) stays local ("Numerical envelope")
-    const int Y1 = (int)min(min((long long)H, (long long)Y0 + (u1 - u)), (long long)Y0 + a.SH);
+    const int Y1 = (int)min(min((long long)a.r1, (long long)Y0 + (u1 - u)), (long long)Y0 + a.SH);
     u += Y1 - Y0;
-    const int bimg = (int)(seg / nstrips), strip = (int)(seg - (long long)bimg * nstrips);
+    const int bl = (int)(seg / nstrips), strip = (int)(seg - (long long)bl * nstrips);
+    const int bimg = a.b0 + bl;
     const int x0 = strip * TW;
     const size_t plane = (size_t)bimg * H * W;
 
@@ -903,7 +914,7 @@ inline void prof_mark(int i, cudaStream_t st) {
 
 template <int RC>
 fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha, float* beta,
-                               cudaStream_t st) {
+                               int b0, int nb, int ty0, int ty1, cudaStream_t st) {
   const bool stage = bounds_smem<RC>(rho, true) <= (size_t)kMaxDynSmem;
   const size_t smem = bounds_smem<RC>(rho, stage);
   static bool attr_set = false;
@@ -916,27 +927,28 @@ fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha,
               "cudaFuncSetAttribute(k_bounds)");
     attr_set = true;
   }
-  dim3 g((p->W + kBT - 1) / kBT, (p->H + kBT - 1) / kBT, p->B);
+  dim3 g((p->W + kBT - 1) / kBT, ty1 - ty0, nb);
   if (stage)
-    k_bounds<RC, true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
+    k_bounds<RC, true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0, ty0);
   else
-    k_bounds<RC, false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm);
+    k_bounds<RC, false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0, ty0);
   FABF_CUDA(cudaGetLastError(), "k_bounds launch");
   return FABF_OK;
 }
 
-fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta,
-                            cudaStream_t st) {
+// rows [64 ty0, 64 ty1) of images [b0, b0 + nb)
+fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0,
+                            int nb, int ty0, int ty1, cudaStream_t st) {
   prof_mark(0, st);
   fabf_status_t s;
   if (rho <= 8)
-    s = launch_bounds_rc<8>(p, img, rho, alpha, beta, st);
+    s = launch_bounds_rc<8>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
   else if (rho <= 24)
-    s = launch_bounds_rc<24>(p, img, rho, alpha, beta, st);
+    s = launch_bounds_rc<24>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
   else if (rho <= 48)
-    s = launch_bounds_rc<48>(p, img, rho, alpha, beta, st);
+    s = launch_bounds_rc<48>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
   else
-    s = launch_bounds_rc<kMaxRho>(p, img, rho, alpha, beta, st);
+    s = launch_bounds_rc<kMaxRho>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
   if (s != FABF_OK) return s;
   prof_mark(1, st);
   prof_mark(2, st);
@@ -968,7 +980,7 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
     grid_cache[dev] = max(1, per_sm) * sms;
     smem_cache[dev] = smem;
   }
-  const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * fa.H;
+  const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * (fa.r1 - fa.r0);
   const int grid = (int)std::min<long long>(grid_cache[dev], strips);
   k_filter<N, E, TW, PPT, WD><<<grid, kThreads, smem, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
@@ -1037,8 +1049,8 @@ fabf_status_t validate_common(Plan* p, int rho) {
   return FABF_OK;
 }
 
-fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const float* sigma,
-                          int rho, int N, float* out, const fabf_diag_t* diag, cudaStream_t st) {
+fabf_status_t validate_filter(Plan* p, const float* img, const float* theta, const float* sigma,
+                              int rho, int N, float* out) {
   fabf_status_t s = validate_common(p, rho);
   if (s != FABF_OK) return s;
   if (N < 0) return fail(FABF_ERR_INVALID_ARGUMENT, "N < 0");
@@ -1050,10 +1062,20 @@ fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const f
   if (overlaps(out, bytes, img, bytes) || overlaps(out, bytes, theta, bytes) ||
       overlaps(out, bytes, sigma, bytes))
     return fail(FABF_ERR_INVALID_ARGUMENT, "out overlaps an input");
+  return FABF_OK;
+}
+
+// The three kernels for images [b0, b0 + nb), rows [64 ty0, min(H, 64 ty1)).
+// Reads input rows up to rho outside the band (the caller guarantees they are
+// in place); writes out, alpha, beta of the band only.
+fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const float* sigma, int rho,
+                          int N, float* out, const fabf_diag_t* diag, int b0, int nb, int ty0,
+                          int ty1, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int), st), "cudaMemsetAsync(fb_count)");
   p->last_stream = st;
-  s = launch_bounds(p, img, rho, p->alpha, p->beta, st);
+  fabf_status_t s = launch_bounds(p, img, rho, p->alpha, p->beta, b0, nb, ty0, ty1, st);
   if (s != FABF_OK) return s;
+  const size_t bytes = sizeof(float) * (size_t)p->B * p->H * p->W;
   if (diag && diag->alpha)
     FABF_CUDA(cudaMemcpyAsync(diag->alpha, p->alpha, bytes, cudaMemcpyDeviceToDevice, st), "copy alpha");
   if (diag && diag->beta)
@@ -1068,7 +1090,10 @@ fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const f
   fa.H = p->H;
   fa.W = p->W;
   fa.rho = rho;
-  fa.B = p->B;
+  fa.B = nb;
+  fa.b0 = b0;
+  fa.r0 = ty0 * kBT;
+  fa.r1 = std::min(p->H, ty1 * kBT);
   fa.TW = (rho <= 64) ? 128 : 64;
   // segment cap (rows): fresh fp64 sums every few window heights
   fa.SH = std::max(64, 3 * (2 * rho + 1));
@@ -1088,7 +1113,15 @@ fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const f
   fa.d_kappa = diag ? diag->kappa : nullptr;
   fa.d_t2n = diag ? diag->t2n : nullptr;
   fa.d_code = diag ? diag->code : nullptr;
-  return launch_filter(fa, N, p->B, st);
+  return launch_filter(fa, N, nb, st);
+}
+
+fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const float* sigma,
+                          int rho, int N, float* out, const fabf_diag_t* diag, cudaStream_t st) {
+  fabf_status_t s = validate_filter(p, img, theta, sigma, rho, N, out);
+  if (s != FABF_OK) return s;
+  return filter_band(p, img, theta, sigma, rho, N, out, diag, 0, p->B, 0,
+                     (p->H + kBT - 1) / kBT, st);
 }
 
 }  // namespace
@@ -1157,11 +1190,17 @@ fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* al
   if (overlaps(alpha, bytes, img, bytes) || overlaps(beta, bytes, img, bytes) ||
       overlaps(alpha, bytes, beta, bytes))
     return fail(FABF_ERR_INVALID_ARGUMENT, "outputs overlap");
-  return launch_bounds(p, img, rho, alpha, beta, (cudaStream_t)stream);
+  return launch_bounds(p, img, rho, alpha, beta, 0, p->B, 0, (p->H + kBT - 1) / kBT,
+                       (cudaStream_t)stream);
 }
 
 fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
                                const float* sigma, int rho, int N, float* out, void* stream) {
+  // Host buffers in and out, pipelined by row bands (multiples of the 64-row
+  // bounds tiles): band k's inputs go up on a copy stream, its kernels run on
+  // `stream` once bands k and k+1 (its rho-row halo) are resident, and its
+  // output comes back on a second copy stream, so the PCIe transfers overlap
+  // each other and the kernels.
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p) return fail(FABF_ERR_INVALID_ARGUMENT, "plan is NULL");
   if (!img || !theta || !sigma || !out) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -1171,14 +1210,67 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
     if ((e = cudaMalloc(&p->h_in, 3 * bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
     if ((e = cudaMalloc(&p->h_out, bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
   }
-  cudaStream_t st = (cudaStream_t)stream;
-  FABF_CUDA(cudaMemcpyAsync(p->h_in, img, bytes, cudaMemcpyHostToDevice, st), "H2D img");
-  FABF_CUDA(cudaMemcpyAsync(p->h_in + px, theta, bytes, cudaMemcpyHostToDevice, st), "H2D theta");
-  FABF_CUDA(cudaMemcpyAsync(p->h_in + 2 * px, sigma, bytes, cudaMemcpyHostToDevice, st), "H2D sigma");
-  fabf_status_t s = filter_impl(p, p->h_in, p->h_in + px, p->h_in + 2 * px, rho, N, p->h_out,
-                                nullptr, st);
+  if (!p->cs_in) {
+    FABF_CUDA(cudaStreamCreateWithFlags(&p->cs_in, cudaStreamNonBlocking), "cudaStreamCreate");
+    FABF_CUDA(cudaStreamCreateWithFlags(&p->cs_out, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < kMaxBands + 1; ++i) {
+      FABF_CUDA(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming), "cudaEventCreate");
+      FABF_CUDA(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  float* dimg = p->h_in;
+  float* dth = p->h_in + px;
+  float* dsg = p->h_in + 2 * px;
+  fabf_status_t s = validate_filter(p, dimg, dth, dsg, rho, N, p->h_out);
   if (s != FABF_OK) return s;
-  FABF_CUDA(cudaMemcpyAsync(out, p->h_out, bytes, cudaMemcpyDeviceToHost, st), "D2H out");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int H = p->H, W = p->W;
+  const int ntile = (H + kBT - 1) / kBT;
+  // bands of whole tiles, each at least rho rows (the halo stays in one neighbour)
+  int nband = std::min(kMaxBands, std::max(1, ntile / 2));
+  while (nband > 1 && ((ntile / nband) * kBT < rho + 1)) --nband;
+  int tb[kMaxBands + 1];
+  for (int k = 0; k <= nband; ++k) tb[k] = (int)((long long)ntile * k / nband);
+  // the copy-in stream starts after work already queued on `stream`
+  FABF_CUDA(cudaEventRecord(p->ev_in[kMaxBands], st), "cudaEventRecord");
+  FABF_CUDA(cudaStreamWaitEvent(p->cs_in, p->ev_in[kMaxBands], 0), "cudaStreamWaitEvent");
+  for (int b = 0; b < p->B; ++b) {
+    const size_t plane = (size_t)b * H * W;
+    for (int k = 0; k < nband; ++k) {
+      const int r0 = tb[k] * kBT, r1 = std::min(H, tb[k + 1] * kBT);
+      const size_t o = plane + (size_t)r0 * W, nbytes = sizeof(float) * (size_t)(r1 - r0) * W;
+      FABF_CUDA(cudaMemcpyAsync(dimg + o, img + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D img");
+      FABF_CUDA(cudaMemcpyAsync(dth + o, theta + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D theta");
+      FABF_CUDA(cudaMemcpyAsync(dsg + o, sigma + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D sigma");
+      FABF_CUDA(cudaEventRecord(p->ev_in[k], p->cs_in), "cudaEventRecord");
+      if (k >= 1 || nband == 1) {
+        const int kc = (nband == 1) ? 0 : k - 1;  // band kc now has its halo
+        FABF_CUDA(cudaStreamWaitEvent(st, p->ev_in[k], 0), "cudaStreamWaitEvent");
+        s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[kc], tb[kc + 1], st);
+        if (s != FABF_OK) return s;
+        FABF_CUDA(cudaEventRecord(p->ev_done[kc], st), "cudaEventRecord");
+        const int q0 = tb[kc] * kBT, q1 = std::min(H, tb[kc + 1] * kBT);
+        const size_t oo = plane + (size_t)q0 * W;
+        FABF_CUDA(cudaStreamWaitEvent(p->cs_out, p->ev_done[kc], 0), "cudaStreamWaitEvent");
+        FABF_CUDA(cudaMemcpyAsync(out + oo, p->h_out + oo, sizeof(float) * (size_t)(q1 - q0) * W,
+                                  cudaMemcpyDeviceToHost, p->cs_out),
+                  "D2H out");
+      }
+    }
+    if (nband > 1) {  // last band of the frame
+      const int kc = nband - 1;
+      s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[kc], tb[kc + 1], st);
+      if (s != FABF_OK) return s;
+      FABF_CUDA(cudaEventRecord(p->ev_done[kc], st), "cudaEventRecord");
+      const int q0 = tb[kc] * kBT, q1 = H;
+      const size_t oo = plane + (size_t)q0 * W;
+      FABF_CUDA(cudaStreamWaitEvent(p->cs_out, p->ev_done[kc], 0), "cudaStreamWaitEvent");
+      FABF_CUDA(cudaMemcpyAsync(out + oo, p->h_out + oo, sizeof(float) * (size_t)(q1 - q0) * W,
+                                cudaMemcpyDeviceToHost, p->cs_out),
+                "D2H out");
+    }
+  }
+  FABF_CUDA(cudaStreamSynchronize(p->cs_out), "cudaStreamSynchronize");
   FABF_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   return FABF_OK;
 }
@@ -1240,6 +1332,16 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   cudaFree(p->fb_list);
   cudaFree(p->h_in);
   cudaFree(p->h_out);
+  if (p->cs_in) {
+    cudaStreamSynchronize(p->cs_in);
+    cudaStreamSynchronize(p->cs_out);
+    cudaStreamDestroy(p->cs_in);
+    cudaStreamDestroy(p->cs_out);
+    for (int i = 0; i < kMaxBands + 1; ++i) {
+      cudaEventDestroy(p->ev_in[i]);
+      cudaEventDestroy(p->ev_done[i]);
+    }
+  }
   delete p;
   return FABF_OK;
 }
