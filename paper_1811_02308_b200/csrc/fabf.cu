@@ -12,7 +12,9 @@
 //       registers (fabf_device.cuh).
 //   k_fallback<N> -- pixels whose centring amplification is too large get
 //       exact direct window Legendre moments (one warp per pixel).
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -41,6 +43,11 @@ struct fabf_plan_s {
   float* h_in = nullptr;  // device staging for fabf_filter_host
   float* h_out = nullptr;
   void* last_stream = nullptr;
+  // TMA descriptor of the last image k_bounds staged (per rho class)
+  CUtensorMap tmap;
+  const void* tmap_ptr = nullptr;
+  int tmap_rc = -1;
+  bool tmap_ok = false;
   // fabf_filter_host pipeline: copy streams and per-band events
   static constexpr int kMaxBandsPlan = 8;
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
@@ -281,19 +288,51 @@ __device__ __forceinline__ void vhgw_run(const TIn* __restrict__ in, float2* __r
   }
 }
 
+// TMA (cp.async.bulk.tensor) staging of an interior footprint: one thread
+// issues the 3-D box load, the CTA waits on an mbarrier.
+__device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, int x, int y, int b,
+                                             unsigned long long* bar, unsigned bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(d),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(b), "r"(mb)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(mb), "r"(parity)
+        : "memory");
+  }
+}
+
 // shared memory: F (staged footprint, fp32, row pitch FP; reused as O after
 // pass V) and Vm (row pitch VP, odd).  Pitches are compile-time per rho class
 // RC (rho <= RC) so that every walk address is a base plus an immediate.
 template <int RC>
 struct BoundsGeom {
-  static constexpr int FP = kBT + 2 * RC;        // >= footprint columns
+  static constexpr int FP = kBT + 2 * RC + 4;    // >= footprint columns + TMA start alignment
+  static constexpr int FR = kBT + 2 * RC;        // TMA box rows
   static constexpr int VP = (kBT + 2 * RC) | 1;  // odd: pass-H lanes (rows) conflict-free
   static constexpr int OP = kBT + 1;
 };
 template <int RC>
 __host__ __device__ inline size_t bounds_f_bytes(int rho, bool stage) {
   using G = BoundsGeom<RC>;
-  const size_t f = stage ? sizeof(float) * (size_t)(kBT + 2 * rho) * G::FP : 0;
+  // staged: room for the whole TMA box (FR rows x FP) of interior tiles
+  const size_t f = stage ? sizeof(float) * (size_t)G::FP * G::FR : 0;
   const size_t o = sizeof(float2) * (size_t)kBT * G::OP;
   return ((f > o ? f : o) + 15) & ~(size_t)15;
 }
@@ -306,10 +345,13 @@ template <int RC, bool kStage>
 __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ img, int H, int W,
                                                       int rho, float* __restrict__ amin,
                                                       float* __restrict__ bmax,
-                                                      float2* __restrict__ blkmm, int b0, int ty0) {
+                                                      float2* __restrict__ blkmm, int b0, int ty0,
+                                                      const __grid_constant__ CUtensorMap tmap,
+                                                      int use_tma) {
   using G = BoundsGeom<RC>;
+  __shared__ __align__(8) unsigned long long tbar;
   constexpr int FP = G::FP, VP = G::VP, OP = G::OP;
-  extern __shared__ __align__(16) unsigned char smb[];
+  extern __shared__ __align__(1024) unsigned char smb[];
   __shared__ float2 red[kThreads / 32];
   const int w = 2 * rho + 1;
   float* F = reinterpret_cast<float*>(smb);                                  // [ny + 2 rho][FP]
@@ -325,7 +367,19 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
   const int tid = threadIdx.x;
   const float* src = img + plane;
 
-  if (kStage) {  // coalesced staging of the footprint, many loads in flight
+  const bool interior_tile = x0 - rho >= 0 && x0 + nx + rho <= W && y0 - rho >= 0 && y0 + ny + rho <= H;
+  if (kStage && use_tma && interior_tile) {
+    // one TMA box load; the box starts at a 16-byte aligned column (a TMA
+    // requirement), the footprint then sits delta columns into each row
+    const int xs = (x0 - rho) & ~3, delta = (x0 - rho) - xs;
+    if (tid == 0) {
+      mbar_init(&tbar, 1);
+      tma_load_box(F, &tmap, xs, y0 - rho, bimg, &tbar, sizeof(float) * FP * G::FR);
+    }
+    __syncthreads();  // mbarrier initialised before anyone polls it
+    mbar_wait(&tbar, 0);
+    F += delta;
+  } else if (kStage) {  // coalesced staging of the footprint, many loads in flight
     // cp.async (LDGSTS): every element in flight at once, no register round trip
     constexpr int kCU = (kBT + 2 * RC + 31) / 32;  // 32-column chunks per row, max
     const int lane = tid & 31;
@@ -927,11 +981,42 @@ fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha,
               "cudaFuncSetAttribute(k_bounds)");
     attr_set = true;
   }
+  // TMA descriptor for interior tiles (needs 16-byte row pitch); encoded
+  // once per (image pointer, rho class) through the runtime's driver entry point
+  if (stage && (p->tmap_ptr != img || p->tmap_rc != RC)) {
+    p->tmap_ptr = img;
+    p->tmap_rc = RC;
+    p->tmap_ok = false;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      else
+        cudaGetLastError();
+    }
+    constexpr cuuint32_t FPB = (cuuint32_t)BoundsGeom<RC>::FP, FRB = (cuuint32_t)BoundsGeom<RC>::FR;
+    if (encode && p->W % 4 == 0 && FPB <= 256 && FRB <= 256) {
+      const cuuint64_t dims[3] = {(cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->B};
+      const cuuint64_t strides[2] = {(cuuint64_t)p->W * 4, (cuuint64_t)p->W * p->H * 4};
+      const cuuint32_t box[3] = {FPB, FRB, 1};
+      const cuuint32_t es[3] = {1, 1, 1};
+      p->tmap_ok = encode(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(img), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
+  const int use_tma = (stage && p->tmap_ok) ? 1 : 0;
   dim3 g((p->W + kBT - 1) / kBT, ty1 - ty0, nb);
   if (stage)
-    k_bounds<RC, true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0, ty0);
+    k_bounds<RC, true><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0, ty0,
+                                                  p->tmap, use_tma);
   else
-    k_bounds<RC, false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0, ty0);
+    k_bounds<RC, false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0,
+                                                   ty0, p->tmap, 0);
   FABF_CUDA(cudaGetLastError(), "k_bounds launch");
   return FABF_OK;
 }

@@ -51,7 +51,10 @@ def _run(fb, w, flags=0, diag=False):
 # ------------------------------------------------------------------ step a1
 @pytest.mark.parametrize("shape,rho", [
     ((1, 1, 1), 0), ((1, 7, 7), 3), ((2, 37, 53), 5), ((1, 64, 300), 20), ((1, 300, 41), 20),
-    ((3, 97, 129), 2), ((1, 200, 333), 40), ((1, 193, 517), 96), ((1, 256, 256), 0)])
+    ((3, 97, 129), 2), ((1, 200, 333), 40), ((1, 193, 517), 96), ((1, 256, 256), 0),
+    # width % 4 == 0: interior tiles staged by TMA from a 16-byte aligned column
+    ((1, 256, 256), 9), ((1, 192, 320), 10), ((2, 200, 260), 11), ((1, 300, 512), 24),
+    ((1, 260, 388), 33)])
 def test_bounds_bit_exact(fb, orc, shape, rho):
     import torch
 
