@@ -133,7 +133,8 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
   const double E = exp_nonpos(qn - qf);        // <= 1
   const bool inside = (xa >= 0.0) && (xb >= 0.0);
   const double Gn = exp_nonpos(inside ? -qn : 0.0);  // scale 1 inside, exp(qn) outside
-  const double ca = erfcx_pos(fabs(xa)), cb = erfcx_pos(fabs(xb));
+  double ca, cb;
+  erfcx_pos2(fabs(xa), fabs(xb), ca, cb);
   const double cn = a_near ? ca : cb, cf = a_near ? cb : ca;
   const double gn = Gn, gf = Gn * E;
   // erf(xa) + erf(xb): inside 2 - erfc(xa) - erfc(xb); outside erfc(|x_near|) - erfc(x_far)
@@ -306,10 +307,12 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     res.code |= kCodeSmallLambda;
     scale_log = -0.69314718055994530942;  // A = J here
   } else if (regime == kRegA) {
-    const double da = (double)alpha, db = (double)beta, d = db - da, rd = rcp64(d);
+    const double da = (double)alpha, db = (double)beta, d = db - da;
     const double sg = (double)sigma;
+    const double rds = rcp64(d * sg);  // one reciprocal for 1/d and 1/sigma
+    const double rd = sg * rds;
     const double s0 = fma(2.0, (double)theta, -(da + db)) * rd;
-    const double sk = 0.35355339059327376220 * d * rcp64(sg);  // d / (2 sqrt2 sigma)
+    const double sk = 0.35355339059327376220 * d * (d * rds);  // d / (2 sqrt2 sigma)
     const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
     const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
     double T2, U, ab, A0, X0;
@@ -332,10 +335,10 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
   }
   float ratio;
   if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {
-    ratio = X0f / A0f;
+    ratio = __fdividef(X0f, A0f);
     res.code |= kCodeGuard;
   } else {
-    ratio = Uf / T2f;
+    ratio = __fdividef(Uf, T2f);  // (2 ulp: the sums carry the cancellation, not the ratio)
   }
   res.kappa = (T2f > 0.0f) ? abf / T2f : CUDART_INF_F;
   // T2 / n in the units of eq.(29) (J = A/2, unscaled)
