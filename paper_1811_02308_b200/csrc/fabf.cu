@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -59,6 +60,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxBands = fabf_plan_s::kMaxBandsPlan;  // fabf_filter_host row bands
+constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds fused into k_filter
+bool g_no_fuse = getenv("FABF_NO_FUSE") != nullptr;  // A/B switch for experiments
 #ifndef FABF_FILTER_MINB
 #define FABF_FILTER_MINB 2
 #endif
@@ -479,8 +482,11 @@ struct FilterArgs {
   const float* alpha;
   const float* beta;
   float* out;
+  float* alpha_w;  // fused small-rho path: alpha / beta of fallback pixels
+  float* beta_w;
   int B, H, W, rho, TW, SH;
   int b0, r0, r1;  // images [b0, b0 + B), rows [r0, r1) of each (row bands)
+  int fused;       // 1: bounds computed inside k_filter (rho <= kFuseRho)
   const float2* blkmm;  // per kBT x kBT bounds tile: (min alpha, max beta)
   unsigned flags;
   double flag_root;  // 2^(flag_bits / N)
@@ -501,8 +507,8 @@ struct FilterGeom {
 template <int N, int E>
 struct FilterSmem {
   // byte offsets into dynamic shared memory
-  size_t ps, vs, qnu, qth, qsg, qal, qbe, qo, total;
-  __host__ __device__ FilterSmem(int L, int RB, int QS) {
+  size_t ps, vs, qnu, qth, qsg, qal, qbe, qo, ring, vmm, total;
+  __host__ __device__ FilterSmem(int L, int RB, int QS, int WF = 0) {
     using G = FilterGeom<N, E>;
     size_t off = 0;
     ps = off;
@@ -523,11 +529,18 @@ struct FilterSmem {
     off += sizeof(float) * QS;
     qo = off;
     off += sizeof(int) * QS;
+    // fused bounds (WF = 2 rho + 1 > 0): per-column ring of the last WF rows,
+    // and the vertical (min, max) of each step row
+    ring = off;
+    off += sizeof(float) * (size_t)L * WF;
+    off = (off + 7) & ~(size_t)7;
+    vmm = off;
+    off += WF > 0 ? sizeof(float2) * (size_t)RB * L : 0;
     total = off;
   }
 };
 
-template <int N, int E, int TW, int PPT, int WD>
+template <int N, int E, int TW, int PPT, int WD, int WF>
 __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int cntA[2], cntBC[2];
@@ -540,7 +553,9 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   const int H = a.H, W = a.W;
   const int L = TW + 2 * rho;  // input columns of a strip, <= 16 * E (host picks E)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const FilterSmem<N, E> lay(L, RB, QS);
+  const FilterSmem<N, E> lay(L, RB, QS, WF);
+  float* ring = reinterpret_cast<float*>(smraw + lay.ring);    // [L][WF]
+  float2* vmm = reinterpret_cast<float2*>(smraw + lay.vmm);    // [RB][L]
   double* Ps = reinterpret_cast<double*>(smraw + lay.ps);    // [RB][NN][PSQ]
   double* Vs = reinterpret_cast<double*>(smraw + lay.vs);    // [L][VST]
   double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [N+1][QS]
@@ -588,7 +603,19 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     // ---- tile-local centre c_T and power-of-two scale s_T: min/max over the
     // ---- segment's bounds tiles (their windows cover the segment footprint)
     float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
-    {
+    if (WF > 0) {
+      // fused bounds: no bounds tiles -- the range of the segment's input
+      // footprint (rows Y0-rho-1 .. Y1+rho-1 of this thread's column)
+      if (tid < L) {
+        const float* cp = a.img + plane + reflect_index(min(x0 - rho + tid, W - 1 + rho), W);
+#pragma unroll 4
+        for (int y = Y0 - rho - 1; y < Y1 + rho; ++y) {
+          const float v = __ldg(cp + reflect_index(y, H) * W);
+          lmin = fminf(lmin, v);
+          lmax = fmaxf(lmax, v);
+        }
+      }
+    } else {
       const int nby = (H + kBT - 1) / kBT, nbx = (W + kBT - 1) / kBT;
       const int by0 = Y0 / kBT, by1 = (Y1 - 1) / kBT;
       const int bx0 = x0 / kBT, bx1 = min(W - 1, x0 + TW - 1) / kBT;
@@ -599,6 +626,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         lmin = fminf(lmin, mm.x);
         lmax = fmaxf(lmax, mm.y);
       }
+    }
+    {
       for (int off = 16; off > 0; off >>= 1) {
         lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
         lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
@@ -633,6 +662,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       for (int q = 0; q < NN; ++q) V[q] = 0.0;
       for (int yin = Y0 - rho - 1; yin < Y0 + rho; ++yin) {
         const float fv = __ldg(colp + reflect_index(yin, H) * W);
+        if (WF > 0 && yin >= Y0 - rho) ring[c * WF + (yin - (Y0 - rho))] = fv;
         const double uu = fma((double)fv, invS, mcs);
         double pu = uu;
 #pragma unroll
@@ -673,8 +703,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         p_al[i] = p_be[i] = p_th[i] = 0.f;
         p_sg[i] = 1.f;
         if (pvalid[i]) {
-          p_al[i] = __ldg(a.alpha + po[i]);
-          p_be[i] = __ldg(a.beta + po[i]);
+          if (WF == 0) {  // (fused bounds: alpha, beta come from vmm in C1)
+            p_al[i] = __ldg(a.alpha + po[i]);
+            p_be[i] = __ldg(a.beta + po[i]);
+          }
           p_th[i] = __ldg(a.theta + po[i]);
           p_sg[i] = __ldg(a.sigma + po[i]);
         }
@@ -709,6 +741,17 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             }
 #pragma unroll
             for (int q = 0; q < N; ++q) psc[(r * NN + q) * PSQ] = V[q];
+            if (WF > 0) {  // fused bounds: the ring now holds the window's WF rows
+              ring[c * WF + (Yb + r + 2 * rho - Y0) % WF] = fin[r];
+              float mn = ring[c * WF], mx = mn;
+#pragma unroll
+              for (int d = 1; d < WF; ++d) {
+                const float v = ring[c * WF + d];
+                mn = fminf(mn, v);
+                mx = fmaxf(mx, v);
+              }
+              vmm[r * L + c] = make_float2(mn, mx);
+            }
           }
         }
 #pragma unroll
@@ -774,6 +817,18 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         int regime = -1;  // -1: no record (invalid, identity or fallback)
         double S[N + 1];
         double au = 0.0, bu = 0.0;
+        if (WF > 0 && pvalid[i]) {  // fused bounds: horizontal min / max of vmm
+          const float2* vr = vmm + (px_r + i * (kThreads / TW)) * L + px_x;
+          float2 m = vr[0];
+#pragma unroll
+          for (int d = 1; d < WF; ++d) {
+            const float2 v = vr[d];
+            m.x = fminf(m.x, v.x);
+            m.y = fmaxf(m.y, v.y);
+          }
+          p_al[i] = m.x;
+          p_be[i] = m.y;
+        }
         if (pvalid[i]) {
           if (p_al[i] == p_be[i]) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
             a.out[po[i]] = p_al[i];
@@ -786,6 +841,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             if (stretch_flagged(au, bu, a.flag_root)) {  // exact-moment fallback pass
               const int slotfb = atomicAdd(a.fb_count, 1);
               a.fb_list[slotfb] = po[i];
+              if (WF > 0) {  // the fallback kernel reads alpha, beta from the plan
+                a.alpha_w[po[i]] = p_al[i];
+                a.beta_w[po[i]] = p_be[i];
+              }
             } else {
               float lam, t0;
               regime = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
@@ -1040,14 +1099,27 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
   return FABF_OK;
 }
 
-#ifndef FABF_PPT
-#define FABF_PPT 2
-#endif
-template <int N, int E, int TW, int WD = 0>
+// pixels per thread per step: 2 when the (worst-case L = 16E) shared memory
+// still fits two CTAs per SM, else 1
+template <int N, int E, int WF>
+constexpr int ppt_for() {
+  constexpr int NN = N > 0 ? N : 1;
+  constexpr size_t L = (size_t)kSL * E;
+  constexpr size_t ps2 = sizeof(double) * 4 * NN * (L + 2);
+  constexpr size_t vs = sizeof(double) * (NN | 1) * L;
+  constexpr size_t q2 = (sizeof(double) * (N + 1) + 5 * 4) * 2 * kThreads;
+  constexpr size_t fz = sizeof(float) * L * WF + (WF > 0 ? sizeof(float2) * 4 * L : 0);
+  return ps2 + vs + q2 + fz <= 110 * 1024 ? 2 : 1;
+}
+template <int N, int E, int TW, int WD = 0, int WF = 0>
 fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
+#ifdef FABF_PPT
   constexpr int PPT = FABF_PPT;
+#else
+  constexpr int PPT = ppt_for<N, E, WF>();
+#endif
   const int L = TW + 2 * fa.rho, QS = PPT * kThreads, RB = QS / TW;
-  const size_t smem = FilterSmem<N, E>(L, RB, QS).total;
+  const size_t smem = FilterSmem<N, E>(L, RB, QS, WF).total;
   if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
   static int grid_cache[64] = {};  // resident CTAs per device (persistent schedule)
   static size_t smem_cache[64] = {};
@@ -1055,11 +1127,11 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   if (dev < 0 || dev >= 64) dev = 0;
   if (grid_cache[dev] == 0 || smem_cache[dev] != smem) {
-    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT, WD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT, WD, WF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxDynSmem),
               "cudaFuncSetAttribute(k_filter)");
     int per_sm = 0, sms = 0;
-    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT, WD>, kThreads, smem),
+    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT, WD, WF>, kThreads, smem),
               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     FABF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
     grid_cache[dev] = max(1, per_sm) * sms;
@@ -1067,7 +1139,7 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   }
   const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * (fa.r1 - fa.r0);
   const int grid = (int)std::min<long long>(grid_cache[dev], strips);
-  k_filter<N, E, TW, PPT, WD><<<grid, kThreads, smem, st>>>(fa);
+  k_filter<N, E, TW, PPT, WD, WF><<<grid, kThreads, smem, st>>>(fa);
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
   return FABF_OK;
 }
@@ -1079,7 +1151,16 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   fabf_status_t s;
   // prefix rows of 16*E entries, E odd (conflict-free strided phase-B access)
   // (column owners: L = TW + 2 rho <= 256 threads)
-  if (fa.rho <= 3) {  // direct window sums (see k_filter, phase B)
+  if (fa.fused) {  // rho <= 5: bounds fused into k_filter (no k_bounds, no alpha/beta planes)
+    switch (fa.rho) {
+      case 0: s = launch_filter_net<N, 9, 128, 1, 1>(fa, st); break;
+      case 1: s = launch_filter_net<N, 9, 128, 3, 3>(fa, st); break;
+      case 2: s = launch_filter_net<N, 9, 128, 5, 5>(fa, st); break;
+      case 3: s = launch_filter_net<N, 9, 128, 7, 7>(fa, st); break;
+      case 4: s = launch_filter_net<N, 9, 128, 0, 9>(fa, st); break;
+      default: s = launch_filter_net<N, 9, 128, 0, 11>(fa, st); break;
+    }
+  } else if (fa.rho <= 3) {  // direct window sums (see k_filter, phase B)
     switch (fa.rho) {
       case 0: s = launch_filter_net<N, 9, 128, 1>(fa, st); break;
       case 1: s = launch_filter_net<N, 9, 128, 3>(fa, st); break;
@@ -1158,7 +1239,15 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
                           int ty1, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int), st), "cudaMemsetAsync(fb_count)");
   p->last_stream = st;
-  fabf_status_t s = launch_bounds(p, img, rho, p->alpha, p->beta, b0, nb, ty0, ty1, st);
+  // small windows: bounds inside k_filter (north_star (e): each pixel crosses
+  // HBM once); the diagnostic entry point keeps the separate bounds kernel
+  // because it returns the alpha / beta planes
+  const bool fused = rho <= kFuseRho && diag == nullptr && !g_no_fuse;
+  fabf_status_t s = FABF_OK;
+  if (fused)
+    prof_mark(0, st), prof_mark(1, st), prof_mark(2, st);
+  else
+    s = launch_bounds(p, img, rho, p->alpha, p->beta, b0, nb, ty0, ty1, st);
   if (s != FABF_OK) return s;
   const size_t bytes = sizeof(float) * (size_t)p->B * p->H * p->W;
   if (diag && diag->alpha)
@@ -1171,6 +1260,9 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
   fa.sigma = sigma;
   fa.alpha = p->alpha;
   fa.beta = p->beta;
+  fa.alpha_w = p->alpha;
+  fa.beta_w = p->beta;
+  fa.fused = fused ? 1 : 0;
   fa.out = out;
   fa.H = p->H;
   fa.W = p->W;

@@ -181,6 +181,29 @@ def test_edge_shapes(fb, orc, kind, shape, rho, N):
     assert np.array_equal((d["code"] & 1) > 0, ident)
 
 
+@pytest.mark.parametrize("kind,shape,rho,N", [
+    ("cfg1", None, 3, 5), ("cfg2", None, 5, 6),
+    ("rect", (1, 5, 300), 2, 6), ("texture", (1, 131, 257), 5, 8), ("rect", (2, 37, 53), 4, 10),
+    ("rect", (1, 7, 7), 3, 5), ("rect", (1, 1, 1), 0, 4), ("float", (1, 57, 91), 3, 6),
+    ("flat", (1, 40, 40), 1, 5), ("voronoi", (1, 200, 260), 5, 4)])
+def test_fused_small_rho_all_pixels(fb, orc, kind, shape, rho, N):
+    """rho <= 5 without diagnostics: bounds computed inside k_filter (per-column
+    ring + horizontal min/max, no k_bounds, no alpha/beta planes).  Every pixel
+    against the oracle; identity pixels copy f bit-exactly."""
+    if kind == "cfg1":
+        w = workloads.config(1)
+    elif kind == "cfg2":
+        w = workloads.config(2)
+    else:
+        w = workloads.random_case(*shape, seed=11, kind=kind, rho=rho, N=N)
+    out, _, _ = _run(fb, w)
+    o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+    mx, nbad, _ = compare_guarded(out, o, grey_scale(w.img))
+    assert nbad == 0, f"max |delta| = {mx} grey"
+    ident = (o["code"] & 1) > 0
+    assert np.array_equal(out[ident], w.img[ident])
+
+
 def test_rho0_is_exact_copy(fb):
     w = workloads.random_case(2, 33, 17, seed=3, rho=0, N=5)
     out, _, _ = _run(fb, w)
