@@ -1404,7 +1404,7 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   const int H = p->H, W = p->W;
   const int ntile = (H + kBT - 1) / kBT;
   // bands of whole tiles, each at least rho rows (the halo stays in one neighbour)
-  int nband = std::min(kMaxBands, std::max(1, ntile / 2));
+  int nband = std::min(kMaxBands, std::max(1, ntile / 2));  // 2+ tiles per band
   while (nband > 1 && ((ntile / nband) * kBT < rho + 1)) --nband;
   int tb[kMaxBands + 1];
   for (int k = 0; k <= nband; ++k) tb[k] = (int)((long long)ntile * k / nband);

@@ -306,6 +306,19 @@ def test_host_entry_point_matches_oracle(fb, orc, cfg, scale):
     assert np.array_equal(host2, host_out)
 
 
+@pytest.mark.parametrize("rho,N", [(4, 6), (12, 8)])
+def test_host_entry_point_batch(fb, orc, rho, N):
+    """fabf_filter_host on a batch of 3 frames (bands per frame, fused and
+    unfused bounds): every pixel against the oracle."""
+    w = workloads.random_case(3, 300, 260, seed=77 + rho, kind="voronoi", rho=rho, N=N)
+    plan = fb.Plan(*w.shape)
+    host_out = np.empty_like(w.img)
+    fb.filter_host(plan, w.img, w.theta, w.sigma, w.rho, w.N, host_out)
+    o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+    mx, nbad, _ = compare_guarded(host_out, o, 1.0)
+    assert nbad == 0, f"max |delta| = {mx} grey"
+
+
 def test_deterministic_and_stream_safe(fb):
     import torch
 
