@@ -484,7 +484,8 @@ struct FilterArgs {
   float* out;
   float* alpha_w;  // fused small-rho path: alpha / beta of fallback pixels
   float* beta_w;
-  int B, H, W, rho, TW, SH;
+  int B, H, W, rho;
+  int SH;          // segment cap (rows)
   int b0, r0, r1;  // images [b0, b0 + B), rows [r0, r1) of each (row bands)
   int fused;       // 1: bounds computed inside k_filter (rho <= kFuseRho)
   const float2* blkmm;  // per kBT x kBT bounds tile: (min alpha, max beta)
@@ -878,11 +879,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         if (regime >= 0) {
           const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
                                           : QS - 1 - (baseB + __popc(mB & lt));
-#ifdef FABF_SKIP_STRETCH  // timing experiment only
-          for (int k = 0; k <= N; ++k) qnu[k * QS + j] = S[k];
-#else
           nu_from_sums<N>(S, au, bu, qnu + j, QS);
-#endif
           qth[j] = p_th[i];
           qsg[j] = p_sg[i];
           qal[j] = p_al[i];
@@ -902,19 +899,12 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             const double* nu = qnu + j;  // nu[k * QS]
             const int o = qo[j];
             const float th = qth[j], sg = qsg[j], al = qal[j], be = qbe[j];
-#ifdef FABF_SKIP_C2  // timing experiment only: no integrals / ratio
-            PixelResult res;
-            res.g = (float)(nu[0] + nu[N * QS]) + th + sg;
-            res.kappa = res.t2n = 0.f;
-            res.code = 0;
-#else
             int regime = kRegA;
             if (j >= nA) {
               float lam, t0;
               regime = range_params(al, be, th, sg, lam, t0);
             }
             PixelResult res = ghat_from_record<N>(nu, QS, th, sg, al, be, regime, a.flags, want_t2n, n);
-#endif
             a.out[o] = res.g;
             if (a.d_kappa) a.d_kappa[o] = res.kappa;
             if (a.d_t2n) a.d_t2n[o] = res.t2n;
@@ -1271,7 +1261,6 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
   fa.b0 = b0;
   fa.r0 = ty0 * kBT;
   fa.r1 = std::min(p->H, ty1 * kBT);
-  fa.TW = (rho <= 64) ? 128 : 64;
   // segment cap (rows): fresh fp64 sums every few window heights
   fa.SH = std::max(64, 3 * (2 * rho + 1));
   fa.blkmm = p->blkmm;
