@@ -319,6 +319,32 @@ def test_host_entry_point_batch(fb, orc, rho, N):
     assert nbad == 0, f"max |delta| = {mx} grey"
 
 
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_cuda_graph_capture_and_replay(fb, cfg):
+    """fabf_filter is graph-capturable (include/fabf.h): capture one call on a
+    side stream, replay it, and get the eager result bit-exactly (fused and
+    separate-bounds paths)."""
+    import torch
+
+    w = workloads.config(cfg, scale=0.5)
+    plan = fb.Plan(*w.shape)
+    img, th, sg = _dev(w.img), _dev(w.theta), _dev(w.sigma)
+    ref = fb.filter(plan, img, th, sg, w.rho, w.N)
+    out = torch.empty_like(img)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fb.filter(plan, img, th, sg, w.rho, w.N, out=out)  # warm-up on the capture stream
+        s.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fb.filter(plan, img, th, sg, w.rho, w.N, out=out, stream=s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+
+
 def test_deterministic_and_stream_safe(fb):
     import torch
 
