@@ -63,8 +63,9 @@ typedef enum {
 
 typedef struct fabf_plan_s* fabf_plan_t;
 
-/* Create a plan for images of shape batch x height x width (all >= 1).
- * Allocates the plan's device workspace (the list of pixels flagged for the
+/* Create a plan for images of shape batch x height x width (all >= 1,
+ * batch*height*width < 2^31).  Allocates the plan's device workspace (alpha /
+ * beta planes, per-64x64-tile bounds, the list of pixels flagged for the
  * exact-moment fallback and its counter) on the current device; no allocation
  * happens later in fabf_filter.  flags: FABF_FLAG_* (0 = guarded, unclamped).
  * Returns FABF_ERR_UNSUPPORTED when the current device is not compute
@@ -74,10 +75,14 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
 /* The filter.  img, theta, sigma, out: DEVICE pointers (float32,
  * batch*height*width, 16-byte aligned); out must not overlap any input.
  * rho >= 0 with 2*rho+1 <= min(height, width); 0 <= N <= FABF_MAX_N.
- * rho == 0 is an exact copy (every window is a single sample).
+ * rho == 0 is an exact copy (every window is a single sample); rho <= 96.
  * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous, does
  * not synchronise and does not read device memory on the host; capturable
- * into a CUDA graph.                                                           */
+ * into a CUDA graph (tests/test_gpu_parity.py replays a captured call).
+ * Kernels: rho <= 5 -> one fused kernel (bounds computed inside it) plus the
+ * fallback kernel; rho > 5 -> bounds kernel, filter kernel, fallback kernel.
+ * The output may differ from fabf_filter_host / fabf_filter_diag in the last
+ * bits (segment boundaries set the tile-local centring).        */
 fabf_status_t fabf_filter(fabf_plan_t plan, const float* img, const float* theta,
                           const float* sigma, int rho, int N, float* out, void* stream);
 
@@ -104,9 +109,13 @@ fabf_status_t fabf_filter_diag(fabf_plan_t plan, const float* img, const float* 
 fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* alpha,
                           float* beta, void* stream);
 
-/* End-to-end convenience: HOST pointers (pinned memory recommended).  Copies
- * the inputs to plan-owned device buffers, runs fabf_filter, copies out back,
- * all enqueued on stream; synchronises the stream before returning.          */
+/* End-to-end convenience: HOST pointers (pinned memory recommended: pageable
+ * memory serialises the copies).  Copies the inputs to plan-owned device
+ * buffers (allocated on first use) and the result back, pipelined by row
+ * bands of whole 64-row tiles: inputs on a plan-owned copy stream, the
+ * kernels of band k on `stream` once band k+1 (its rho-row halo) is resident,
+ * the output of band k on a second copy stream.  Synchronises before
+ * returning.  Same argument rules and errors as fabf_filter.                  */
 fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
                                const float* sigma, int rho, int N, float* out, void* stream);
 
