@@ -661,15 +661,29 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       double V[NN];
 #pragma unroll
       for (int q = 0; q < NN; ++q) V[q] = 0.0;
-      for (int yin = Y0 - rho - 1; yin < Y0 + rho; ++yin) {
-        const float fv = __ldg(colp + reflect_index(yin, H) * W);
-        if (WF > 0 && yin >= Y0 - rho) ring[c * WF + (yin - (Y0 - rho))] = fv;
-        const double uu = fma((double)fv, invS, mcs);
-        double pu = uu;
+      // rows in batches of 8 loads issued ahead of the arithmetic (the loop is
+      // otherwise one exposed L2 latency per row)
+      constexpr int PB = 8;
+      for (int y0 = Y0 - rho - 1; y0 < Y0 + rho; y0 += PB) {
+        float fb[PB];
 #pragma unroll
-        for (int q = 0; q < N; ++q) {
-          V[q] += pu;
-          pu *= uu;
+        for (int k = 0; k < PB; ++k) {
+          const int yin = min(y0 + k, Y0 + rho - 1);
+          fb[k] = __ldg(colp + reflect_index(yin, H) * W);
+        }
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          const int yin = y0 + k;
+          if (yin < Y0 + rho) {
+            if (WF > 0 && yin >= Y0 - rho) ring[c * WF + (yin - (Y0 - rho))] = fb[k];
+            const double uu = fma((double)fb[k], invS, mcs);
+            double pu = uu;
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+              V[q] += pu;
+              pu *= uu;
+            }
+          }
         }
       }
 #pragma unroll
