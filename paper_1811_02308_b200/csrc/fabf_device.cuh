@@ -198,7 +198,7 @@ __device__ __forceinline__ void integrals_regime_b(float lam, float t0, float A[
 // support [a,b] of the integrand (truncated where it has decayed by e^-24 from
 // its value at the nearer end of [0,1]), fp64, scaled by exp(lambda d^2).
 template <int N>
-__device__ __noinline__ void integrals_regime_c(double lam, double t0, double A[N + 1],
+__device__ __forceinline__ void integrals_regime_c(double lam, double t0, double A[N + 1],
                                                 double X[N + 1]) {
   double a, b, d;
   if (t0 < 0.0) {
@@ -323,7 +323,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
       scale_log = (xa >= 0.0 && xb >= 0.0) ? 0.0 : fmin(xa * xa, xb * xb);
     }
   } else {
-    double A[N + 1], X[N + 1];  // (local memory: the regime-C call is out of line)
+    double A[N + 1], X[N + 1];
     const double da = (double)alpha, db = (double)beta, d = db - da;
     const double t0 = ((double)theta - da) / d;
     const double r = d / (double)sigma, lam = 0.5 * r * r;
