@@ -780,6 +780,34 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         // without a row of its own re-scans its partner's and does not store.
         // Two rows per group and pass (s0, s0 + 16): two independent add chains.
         constexpr int G = kThreads / kSL;  // 16 groups
+        if (E > 13) {  // wide rows: one scan per pass (two would spill)
+          for (int b = 2 * warp; b < nr * N; b += G) {
+            const int s0 = b + (sgrp & 1);
+            const bool act0 = s0 < nr * N;
+            double* row0 = Ps + (act0 ? s0 : b) * PSQ + 1 + sl * E;
+            double v0[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) v0[e] = row0[e];
+            double t0 = 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              t0 += v0[e];
+              v0[e] = t0;
+            }
+            double i0 = t0;
+#pragma unroll
+            for (int off = 1; off < kSL; off <<= 1) {
+              const double u0 = __shfl_up_sync(0xffffffffu, i0, off, kSL);
+              if (sl >= off) i0 += u0;
+            }
+            double e0 = __shfl_up_sync(0xffffffffu, i0, 1, kSL);
+            if (sl == 0) e0 = 0.0;
+            if (act0) {
+#pragma unroll
+              for (int e = 0; e < E; ++e) row0[e] = v0[e] + e0;
+            }
+          }
+        } else
         for (int b = 2 * warp; b < nr * N; b += 2 * G) {
           const int s0 = b + (sgrp & 1), s1 = s0 + G;
           const bool act0 = s0 < nr * N, act1 = s1 < nr * N;
