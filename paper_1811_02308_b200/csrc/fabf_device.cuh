@@ -124,8 +124,8 @@ __constant__ double c_rec[2 * (kMaxN + 1)] = {
 
 template <int N>
 __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double csk, double inv2k,
-                                                   const double* nup, int ns, double& T2, double& U,
-                                                   double& ab, double& A0, double& X0) {
+                                                   const double* nup, int ns, double nu0, double& T2,
+                                                   double& U, double& ab, double& A0, double& X0) {
   const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);  // s = +1 and s = -1 ends
   const double qa = xa * xa, qb = xb * xb;
   const bool a_near = qa < qb;
@@ -144,7 +144,9 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
   // a8 sums consumed on the fly (no A / X arrays): T2 = sum nup_k A_k,
   // U = sum nup_k X_k, ab = sum |nup_k A_k|
-  T2 = nup[0] * a0;  // (nup[k * ns]: read where used, not held across the seeds)
+  // nup[k * ns], k >= 1: read where used, not held across the seeds;
+  // nup_0 = nu0 = n (the window size) is never stored
+  T2 = nu0 * a0;
   ab = fabs(T2);
   U = 0.0;
   A0 = a0;
@@ -154,7 +156,7 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
     const double bk = (k & 1) ? bnd_odd : bnd_even;
     const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
     if (k == 0) X0 = x;
-    U = fma(nup[k * ns], x, U);
+    U = fma(k == 0 ? nu0 : nup[k * ns], x, U);
     if (k < N) {
       const double a_next = fma(c_rec[2 * k], x, c_rec[2 * k + 1] * a_prev);
       if (k & 1)
@@ -266,13 +268,13 @@ __device__ __forceinline__ int range_params(float alpha, float beta, float theta
 
 // the fp64 sums of a8 (see above), rounded to fp32 once formed
 template <int N>
-__device__ __forceinline__ void contract(const double* nup, int ns, const double A[N + 1],
+__device__ __forceinline__ void contract(const double* nup, int ns, double nu0, const double A[N + 1],
                                          const double X[N + 1], float& T2f, float& Uf, float& abf,
                                          float& A0f, float& X0f) {
   double T2 = 0.0, U = 0.0, ab = 0.0;
 #pragma unroll
   for (int k = 0; k <= N; ++k) {
-    const double nk = nup[k * ns];
+    const double nk = k == 0 ? nu0 : nup[k * ns];
     T2 = fma(nk, A[k], T2);
     ab = fma(fabs(nk), fabs(A[k]), ab);
     U = fma(nk, X[k], U);
@@ -297,7 +299,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     float T2 = 0.0f, U = 0.0f, ab = 0.0f;
 #pragma unroll
     for (int k = 0; k <= N; ++k) {
-      const float v = (float)nup[k * ns];
+      const float v = k == 0 ? n : (float)nup[k * ns];
       const float t = v * A[k];
       T2 += t;
       ab += fabsf(t);
@@ -316,7 +318,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
     const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
     double T2, U, ab, A0, X0;
-    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, ns, T2, U, ab, A0, X0);
+    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, ns, (double)n, T2, U, ab, A0, X0);
     T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A0, X0f = (float)X0;
     if (want_t2n) {
       const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
@@ -331,7 +333,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     res.code |= kCodeFarTheta;
     const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
     scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
-    contract<N>(nup, ns, A, X, T2f, Uf, abf, A0f, X0f);
+    contract<N>(nup, ns, (double)n, A, X, T2f, Uf, abf, A0f, X0f);
   }
   float ratio;
   if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {
@@ -396,7 +398,7 @@ __device__ __forceinline__ void nu_from_sums(double S[N + 1], double au, double 
     p *= ih;
   }
 #pragma unroll
-  for (int k = 0; k <= N; ++k) {  // nup_k = (2k+1) nu_k: the fit's coefficients (a5)
+  for (int k = 1; k <= N; ++k) {  // nup_k = (2k+1) nu_k: the fit's coefficients (a5); nup_0 = n
     double v = 0.0;
 #pragma unroll
     for (int r = k & 1; r <= k; r += 2) v = fma((double)(2 * k + 1) * leg_coef(k, r), S[r], v);
