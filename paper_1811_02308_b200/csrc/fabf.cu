@@ -544,7 +544,7 @@ struct FilterSmem {
 template <int N, int E, int TW, int PPT, int WD, int WF>
 __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ int cntA[2], cntBC[2];
+  __shared__ int cnt[2];  // per step parity: regime-A count (low 16 bits), B/C count (high 16)
   __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
   using G = FilterGeom<N, E>;
   constexpr int NN = G::NN, PSQ = G::PSQ, VST = G::VST;
@@ -727,8 +727,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         }
       }
       if (tid == 0) {
-        cntA[qb] = 0;
-        cntBC[qb] = 0;
+        cnt[qb] = 0;
       }
       // ---- phase A: entering row Yb+r+rho in, leaving row Yb+r-rho-1 out
       if (owner) {
@@ -912,8 +911,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         const unsigned mB = __ballot_sync(0xffffffffu, regime > kRegA);
         int baseA = 0, baseB = 0;
         if (lane == 0) {
-          if (mA) baseA = atomicAdd(&cntA[qb], __popc(mA));
-          if (mB) baseB = atomicAdd(&cntBC[qb], __popc(mB));
+          if (mA | mB) {  // one atomic for both counters (QS <= 512 < 2^16)
+            const int old = atomicAdd(&cnt[qb], __popc(mA) | (__popc(mB) << 16));
+            baseA = old & 0xffff;
+            baseB = old >> 16;
+          }
         }
         baseA = __shfl_sync(0xffffffffu, baseA, 0);
         baseB = __shfl_sync(0xffffffffu, baseB, 0);
@@ -933,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // ---- phase C2: integrals, ratio, guard, store (one regime per warp).  No
       // ---- barrier after it (see FilterSmem: the counters are double buffered).
       {
-        const int nA = cntA[qb], nBC = cntBC[qb];
+        const int nA = cnt[qb] & 0xffff, nBC = cnt[qb] >> 16;
 #pragma unroll 1
         for (int i = 0; i < PPT; ++i) {
           const int j = tid + i * kThreads;
