@@ -909,16 +909,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         }
         const unsigned mA = __ballot_sync(0xffffffffu, regime == kRegA);
         const unsigned mB = __ballot_sync(0xffffffffu, regime > kRegA);
-        int baseA = 0, baseB = 0;
-        if (lane == 0) {
-          if (mA | mB) {  // one atomic for both counters (QS <= 512 < 2^16)
-            const int old = atomicAdd(&cnt[qb], __popc(mA) | (__popc(mB) << 16));
-            baseA = old & 0xffff;
-            baseB = old >> 16;
-          }
-        }
-        baseA = __shfl_sync(0xffffffffu, baseA, 0);
-        baseB = __shfl_sync(0xffffffffu, baseB, 0);
+        int old = 0;  // one atomic for both counters (QS <= 512 < 2^16)
+        if (lane == 0 && (mA | mB)) old = atomicAdd(&cnt[qb], __popc(mA) | (__popc(mB) << 16));
+        old = __shfl_sync(0xffffffffu, old, 0);
+        const int baseA = old & 0xffff, baseB = old >> 16;
         const unsigned lt = (1u << lane) - 1u;
         if (regime >= 0) {
           const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
