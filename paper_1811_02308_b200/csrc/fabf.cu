@@ -62,6 +62,8 @@ constexpr int kThreads = 256;
 constexpr int kMaxBands = fabf_plan_s::kMaxBandsPlan;  // fabf_filter_host row bands
 constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds fused into k_filter
 bool g_no_fuse = getenv("FABF_NO_FUSE") != nullptr;  // A/B switch for experiments
+// k_fallback mode: 0 auto (default), 1 thread per pixel, 2 warp per pixel (A/B switch)
+int g_fb_mode = getenv("FABF_FB_MODE") ? atoi(getenv("FABF_FB_MODE")) : 0;
 #ifndef FABF_FILTER_MINB
 #define FABF_FILTER_MINB 2
 #endif
@@ -958,21 +960,47 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 // exact-moment fallback: nu_k = sum_j P_k(w_j) directly in fp64 over the
 // window of each listed pixel (w_j stretched by the pixel's own alpha, beta:
 // no centring error), then the same per-pixel integrals / ratio as k_filter.
-// kLanes = 1: one thread per pixel (small windows); 32: one warp per pixel,
-// lanes split the window columns.  The Legendre values come from the
-// unnormalised recurrence Q_{k+1} = (2k+1) s Q_k - k^2 Q_{k-1}, Q_k = k! P_k
-// (integer coefficients), divided by k! once at the end.
+// Two modes, chosen per launch from the device-side list length (uniform):
+//   thread mode: one thread per pixel -- many pixels, small windows;
+//   warp mode:   one warp per pixel, the lanes split the flattened window
+//                (coalesced row loads, full lanes) and reduce by shuffles --
+//                short lists (one serial thread per pixel takes 0.93 ms for
+//                416 pixels at rho = 40; a warp per pixel 0.11 ms).
+// The Legendre values come from the unnormalised recurrence
+// Q_{k+1} = (2k+1) s Q_k - k^2 Q_{k-1}, Q_k = k! P_k (integer coefficients),
+// divided by k! once at the end.
 __constant__ double c_inv_fact[kMaxN + 1] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120,
                                              1.0 / 720, 1.0 / 5040, 1.0 / 40320, 1.0 / 362880,
                                              1.0 / 3628800};
-template <int N, int kLanes>
-__global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
-  const int sub = (kLanes == 1) ? 0 : (threadIdx.x & 31);
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / kLanes;
-  const int nw = (gridDim.x * blockDim.x) / kLanes;
+template <int N>
+__device__ __forceinline__ void fb_accumulate(double (&acc)[N + 1], double sv) {
+  double q0 = 1.0, q1 = sv;
+  acc[0] += 1.0;
+  if (N >= 1) acc[1] += sv;
+#pragma unroll
+  for (int k = 1; k < N; ++k) {
+    const double q2 = fma((double)(2 * k + 1) * q1, sv, -(double)(k * k) * q0);
+    acc[k + 1] += q2;
+    q0 = q1;
+    q1 = q2;
+  }
+}
+template <int N>
+__global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
   const int count = *a.fb_count;
   const int rho = a.rho, w = 2 * rho + 1, n = w * w;
   const int H = a.H, W = a.W;
+  const int nthreads = gridDim.x * blockDim.x;
+  // mode 0: auto; 1: thread per pixel; 2: warp per pixel
+  // (measured crossover: a warp per pixel wins while the list is shorter than
+  // ~5 warps' worth per resident warp; longer lists are throughput-bound and
+  // thread mode's neighbouring-pixel loads share L1 lines -- 3.9 vs 6.2 ms
+  // for 198k pixels at rho = 40)
+  const bool warp_mode = mode == 2 || (mode == 0 && count <= 4 * (nthreads / 32));
+  const int lanes = warp_mode ? 32 : 1;
+  const int sub = warp_mode ? (threadIdx.x & 31) : 0;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / lanes;
+  const int nw = nthreads / lanes;
   for (int i = gw; i < count; i += nw) {
     const int o = a.fb_list[i];
     const int b = o / (H * W), rem = o - b * H * W, y = rem / W, x = rem - y * W;
@@ -982,27 +1010,31 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a) {
     double acc[N + 1];
 #pragma unroll
     for (int k = 0; k <= N; ++k) acc[k] = 0.0;
-#pragma unroll 4
-    for (int dy = -rho; dy <= rho; ++dy) {  // (unrolled: several rows' loads in flight)
-      const float* row = img + reflect_index(y + dy, H) * W;
-      for (int dx = -rho + sub; dx <= rho; dx += kLanes) {
-        const double sv = ((double)__ldg(row + reflect_index(x + dx, W)) - mid) * ih;
-        double q0 = 1.0, q1 = sv;
-        acc[0] += 1.0;
-        if (N >= 1) acc[1] += sv;
-#pragma unroll
-        for (int k = 1; k < N; ++k) {
-          const double q2 = fma((double)(2 * k + 1) * q1, sv, -(double)(k * k) * q0);
-          acc[k + 1] += q2;
-          q0 = q1;
-          q1 = q2;
+    if (warp_mode) {
+      // flattened window index j = sub + 32 t -> (dy, dx), advanced incrementally
+      int dy = sub / w, dx = sub - (sub / w) * w;
+      for (int j = sub; j < n; j += 32) {
+        const float* row = img + reflect_index(y - rho + dy, H) * W;
+        const double sv = ((double)__ldg(row + reflect_index(x - rho + dx, W)) - mid) * ih;
+        fb_accumulate<N>(acc, sv);
+        dx += 32;
+        while (dx >= w) {
+          dx -= w;
+          ++dy;
         }
       }
-    }
-    if (kLanes > 1) {
 #pragma unroll
       for (int k = 0; k <= N; ++k)
         for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+    } else {
+#pragma unroll 4
+      for (int dy = -rho; dy <= rho; ++dy) {  // (unrolled: several rows' loads in flight)
+        const float* row = img + reflect_index(y + dy, H) * W;
+        for (int dx = -rho; dx <= rho; ++dx) {
+          const double sv = ((double)__ldg(row + reflect_index(x + dx, W)) - mid) * ih;
+          fb_accumulate<N>(acc, sv);
+        }
+      }
     }
     if (sub == 0) {
       double nu[N + 1];
@@ -1210,7 +1242,7 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   if (s != FABF_OK) return s;
   prof_mark(3, st);
   // one thread per pixel (neighbouring list entries share their windows in L1)
-  k_fallback<N, 1><<<148 * 4, kThreads, 0, st>>>(fa);
+  k_fallback<N><<<148 * 4, kThreads, 0, st>>>(fa, g_fb_mode);
   FABF_CUDA(cudaGetLastError(), "k_fallback launch");
   prof_mark(4, st);
   return FABF_OK;
