@@ -966,23 +966,25 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 //                (coalesced row loads, full lanes) and reduce by shuffles --
 //                short lists (one serial thread per pixel takes 0.93 ms for
 //                416 pixels at rho = 40; a warp per pixel 0.11 ms).
-// The Legendre values come from the unnormalised recurrence
-// Q_{k+1} = (2k+1) s Q_k - k^2 Q_{k-1}, Q_k = k! P_k (integer coefficients),
-// divided by k! once at the end.
-__constant__ double c_inv_fact[kMaxN + 1] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120,
-                                             1.0 / 720, 1.0 / 5040, 1.0 / 40320, 1.0 / 362880,
-                                             1.0 / 3628800};
+// The Legendre values come from the monic recurrence
+// R_{k+1} = s R_k - k^2 / (4k^2 - 1) R_{k-1}, R_k = P_k / m_k with
+// m_k = binom(2k, k) / 2^k (the three-term recurrence of P_k divided by its
+// leading coefficient): one DMUL + one DFMA per degree instead of the
+// two DMULs + DFMA of the (2k+1) s Q_k - k^2 Q_{k-1} form; P_k = m_k R_k once
+// per pixel at the end.
+__constant__ double c_monic_scale[kMaxN + 1] = {1.0, 1.0, 1.5, 2.5, 4.375, 7.875, 14.4375,
+                                                26.8125, 50.2734375, 94.9609375, 180.42578125};
 template <int N>
 __device__ __forceinline__ void fb_accumulate(double (&acc)[N + 1], double sv) {
-  double q0 = 1.0, q1 = sv;
+  double r0 = 1.0, r1 = sv;
   acc[0] += 1.0;
   if (N >= 1) acc[1] += sv;
 #pragma unroll
   for (int k = 1; k < N; ++k) {
-    const double q2 = fma((double)(2 * k + 1) * q1, sv, -(double)(k * k) * q0);
-    acc[k + 1] += q2;
-    q0 = q1;
-    q1 = q2;
+    const double r2 = fma(-(double)(k * k) / (double)(4 * k * k - 1), r0, sv * r1);
+    acc[k + 1] += r2;
+    r0 = r1;
+    r1 = r2;
   }
 }
 template <int N>
@@ -1039,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
     if (sub == 0) {
       double nu[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * c_inv_fact[k] * acc[k];
+      for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * c_monic_scale[k] * acc[k];
       float lam, t0;
       const float th = a.theta[o], sg = a.sigma[o];
       const int regime = range_params(al, be, th, sg, lam, t0);
