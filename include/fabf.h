@@ -112,10 +112,12 @@ fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* al
 /* End-to-end convenience: HOST pointers (pinned memory recommended: pageable
  * memory serialises the copies).  Copies the inputs to plan-owned device
  * buffers (allocated on first use) and the result back, pipelined by row
- * bands of whole 64-row tiles: inputs on a plan-owned copy stream, the
- * kernels of band k on `stream` once band k+1 (its rho-row halo) is resident,
- * the output of band k on a second copy stream.  Synchronises before
- * returning.  Same argument rules and errors as fabf_filter.                  */
+ * bands of whole 64-row tiles (up to 6 per frame, env FABF_HOST_BANDS=1..16
+ * overrides; every band >= rho + 1 rows, the last one the smallest): inputs
+ * on a plan-owned copy stream in the order img_{k+1}, theta_k, sigma_k, the
+ * kernels of band k on `stream` as soon as those are resident, the output of
+ * band k on a second copy stream.  Synchronises before returning.  Same
+ * argument rules and errors as fabf_filter.                                    */
 fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
                                const float* sigma, int rho, int N, float* out, void* stream);
 

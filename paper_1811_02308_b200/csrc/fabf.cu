@@ -50,7 +50,7 @@ struct fabf_plan_s {
   int tmap_rc = -1;
   bool tmap_ok = false;
   // fabf_filter_host pipeline: copy streams and per-band events
-  static constexpr int kMaxBandsPlan = 8;
+  static constexpr int kMaxBandsPlan = 16;
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
   cudaEvent_t ev_in[kMaxBandsPlan + 1] = {};
   cudaEvent_t ev_done[kMaxBandsPlan + 1] = {};
@@ -64,6 +64,8 @@ constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds fused into k_filter
 bool g_no_fuse = getenv("FABF_NO_FUSE") != nullptr;  // A/B switch for experiments
 // k_fallback mode: 0 auto (default), 1 thread per pixel, 2 warp per pixel (A/B switch)
 int g_fb_mode = getenv("FABF_FB_MODE") ? atoi(getenv("FABF_FB_MODE")) : 0;
+// fabf_filter_host row bands per frame (A/B switch FABF_HOST_BANDS, 1..16)
+int g_host_bands = getenv("FABF_HOST_BANDS") ? std::max(1, std::min(16, atoi(getenv("FABF_HOST_BANDS")))) : 6;
 #ifndef FABF_FILTER_MINB
 #define FABF_FILTER_MINB 2
 #endif
@@ -1464,48 +1466,48 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   cudaStream_t st = (cudaStream_t)stream;
   const int H = p->H, W = p->W;
   const int ntile = (H + kBT - 1) / kBT;
-  // bands of whole tiles, each at least rho rows (the halo stays in one neighbour)
-  int nband = std::min(kMaxBands, std::max(1, ntile / 2));  // 2+ tiles per band
-  while (nband > 1 && ((ntile / nband) * kBT < rho + 1)) --nband;
+  // bands of whole tiles, each at least rho + 1 rows (a band's halo then lies
+  // in its two neighbours).  The last band is the smallest allowed (the
+  // pipeline's tail after the final upload is its kernels plus its download);
+  // the others split the remaining tiles evenly.
+  const int minT = (rho + 1 + kBT - 1) / kBT;  // tiles for rho + 1 rows
+  int nband = std::min(g_host_bands, std::max(1, ntile / 2));  // 2+ tiles per band on average
+  int lastT = minT;
+  while (nband > 1 && ((ntile - lastT) / (nband - 1) < minT || ntile - lastT < nband - 1)) --nband;
+  if (nband == 1) lastT = ntile;
   int tb[kMaxBands + 1];
-  for (int k = 0; k <= nband; ++k) tb[k] = (int)((long long)ntile * k / nband);
+  for (int k = 0; k < nband; ++k) tb[k] = (int)((long long)(ntile - lastT) * k / std::max(1, nband - 1));
+  tb[nband] = ntile;
   // the copy-in stream starts after work already queued on `stream`
   FABF_CUDA(cudaEventRecord(p->ev_in[kMaxBands], st), "cudaEventRecord");
   FABF_CUDA(cudaStreamWaitEvent(p->cs_in, p->ev_in[kMaxBands], 0), "cudaStreamWaitEvent");
   for (int b = 0; b < p->B; ++b) {
     const size_t plane = (size_t)b * H * W;
-    for (int k = 0; k < nband; ++k) {
+    auto rows = [&](int k, size_t& o, size_t& nbytes) {
       const int r0 = tb[k] * kBT, r1 = std::min(H, tb[k + 1] * kBT);
-      const size_t o = plane + (size_t)r0 * W, nbytes = sizeof(float) * (size_t)(r1 - r0) * W;
-      FABF_CUDA(cudaMemcpyAsync(dimg + o, img + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D img");
+      o = plane + (size_t)r0 * W;
+      nbytes = sizeof(float) * (size_t)(r1 - r0) * W;
+    };
+    size_t o, nbytes;
+    rows(0, o, nbytes);
+    FABF_CUDA(cudaMemcpyAsync(dimg + o, img + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D img");
+    for (int k = 0; k < nband; ++k) {
+      // upload order f_{k+1}, theta_k, sigma_k: band k's kernels can start as
+      // soon as its own parameters are up (its lower halo, f_{k+1}, came first)
+      if (k + 1 < nband) {
+        rows(k + 1, o, nbytes);
+        FABF_CUDA(cudaMemcpyAsync(dimg + o, img + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D img");
+      }
+      rows(k, o, nbytes);
       FABF_CUDA(cudaMemcpyAsync(dth + o, theta + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D theta");
       FABF_CUDA(cudaMemcpyAsync(dsg + o, sigma + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D sigma");
       FABF_CUDA(cudaEventRecord(p->ev_in[k], p->cs_in), "cudaEventRecord");
-      if (k >= 1 || nband == 1) {
-        const int kc = (nband == 1) ? 0 : k - 1;  // band kc now has its halo
-        FABF_CUDA(cudaStreamWaitEvent(st, p->ev_in[k], 0), "cudaStreamWaitEvent");
-        s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[kc], tb[kc + 1], st);
-        if (s != FABF_OK) return s;
-        FABF_CUDA(cudaEventRecord(p->ev_done[kc], st), "cudaEventRecord");
-        const int q0 = tb[kc] * kBT, q1 = std::min(H, tb[kc + 1] * kBT);
-        const size_t oo = plane + (size_t)q0 * W;
-        FABF_CUDA(cudaStreamWaitEvent(p->cs_out, p->ev_done[kc], 0), "cudaStreamWaitEvent");
-        FABF_CUDA(cudaMemcpyAsync(out + oo, p->h_out + oo, sizeof(float) * (size_t)(q1 - q0) * W,
-                                  cudaMemcpyDeviceToHost, p->cs_out),
-                  "D2H out");
-      }
-    }
-    if (nband > 1) {  // last band of the frame
-      const int kc = nband - 1;
-      s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[kc], tb[kc + 1], st);
+      FABF_CUDA(cudaStreamWaitEvent(st, p->ev_in[k], 0), "cudaStreamWaitEvent");
+      s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[k], tb[k + 1], st);
       if (s != FABF_OK) return s;
-      FABF_CUDA(cudaEventRecord(p->ev_done[kc], st), "cudaEventRecord");
-      const int q0 = tb[kc] * kBT, q1 = H;
-      const size_t oo = plane + (size_t)q0 * W;
-      FABF_CUDA(cudaStreamWaitEvent(p->cs_out, p->ev_done[kc], 0), "cudaStreamWaitEvent");
-      FABF_CUDA(cudaMemcpyAsync(out + oo, p->h_out + oo, sizeof(float) * (size_t)(q1 - q0) * W,
-                                cudaMemcpyDeviceToHost, p->cs_out),
-                "D2H out");
+      FABF_CUDA(cudaEventRecord(p->ev_done[k], st), "cudaEventRecord");
+      FABF_CUDA(cudaStreamWaitEvent(p->cs_out, p->ev_done[k], 0), "cudaStreamWaitEvent");
+      FABF_CUDA(cudaMemcpyAsync(out + o, p->h_out + o, nbytes, cudaMemcpyDeviceToHost, p->cs_out), "D2H out");
     }
   }
   FABF_CUDA(cudaStreamSynchronize(p->cs_out), "cudaStreamSynchronize");
