@@ -353,11 +353,16 @@ def test_host_entry_point_matches_oracle(fb, orc, cfg, scale):
     assert np.array_equal(host2, host_out)
 
 
-@pytest.mark.parametrize("rho,N", [(4, 6), (12, 8)])
-def test_host_entry_point_batch(fb, orc, rho, N):
-    """fabf_filter_host on a batch of 3 frames (bands per frame, fused and
-    unfused bounds): every pixel against the oracle."""
-    w = workloads.random_case(3, 300, 260, seed=77 + rho, kind="voronoi", rho=rho, N=N)
+@pytest.mark.parametrize("B,H,W,rho,N", [(3, 300, 260, 4, 6), (3, 300, 260, 12, 8),
+                                         # last band a single row (H = 9 * 64 + 1), rho 40
+                                         (1, 577, 200, 40, 6),
+                                         # rho + 1 > 64: bands of two tiles or more
+                                         (2, 420, 150, 70, 4)])
+def test_host_entry_point_batch(fb, orc, B, H, W, rho, N):
+    """fabf_filter_host on batches and band-partition edge cases (bands per
+    frame, fused and unfused bounds, a one-row last band, halos wider than a
+    tile): every pixel against the oracle."""
+    w = workloads.random_case(B, H, W, seed=77 + rho, kind="voronoi", rho=rho, N=N)
     plan = fb.Plan(*w.shape)
     host_out = np.empty_like(w.img)
     fb.filter_host(plan, w.img, w.theta, w.sigma, w.rho, w.N, host_out)
