@@ -750,12 +750,18 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           if (r < nr) {
             const double ui = fma((double)fin[r], invS, mcs);
             const double uo = fma((double)fout[r], invS, mcs);
-            double pu = ui, po2 = uo;
+            // d_q = ui^q - uo^q by its own recurrence d_{q+1} = (ui + uo) d_q
+            // - ui uo d_{q-1} (d_0 = 0): one DMUL + one DFMA per power instead
+            // of two DMULs and a DADD
+            const double sp = ui + uo, pp = ui * uo;
+            double dm = ui - uo, d = sp * dm;  // d_1, d_2
+            if (N >= 1) V[0] += dm;
 #pragma unroll
-            for (int q = 0; q < N; ++q) {
-              V[q] += pu - po2;
-              pu *= ui;
-              po2 *= uo;
+            for (int q = 1; q < N; ++q) {
+              V[q] += d;
+              const double dn = fma(sp, d, -pp * dm);
+              dm = d;
+              d = dn;
             }
 #pragma unroll
             for (int q = 0; q < N; ++q) psc[(r * NN + q) * PSQ] = V[q];
