@@ -53,6 +53,8 @@ typedef enum {
 /* plan flags */
 #define FABF_FLAG_LITERAL 0x1u /* eq.(29) exactly as printed: no guard (reading R7)       */
 #define FABF_FLAG_CLAMP 0x2u   /* clamp g-hat to [alpha_i, beta_i] after the guard (reading R7)    */
+#define FABF_FLAG_DEBUG 0x4u   /* validate the preconditions on the device every call: f, theta
+                                  finite, sigma finite and > 0 (fabf_debug_status reads the result) */
 
 /* per-pixel diagnostic code bits (fabf_diag_t.code) */
 #define FABF_CODE_IDENTITY 0x1u /* alpha == beta: g-hat = f(i)                               */
@@ -124,6 +126,16 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
 /* Number of pixels the last fabf_filter* call on this plan routed to the
  * exact-moment fallback (synchronises the plan's stream to read it).         */
 fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count);
+
+/* FABF_FLAG_DEBUG plans only: the device-side precondition check of the last
+ * fabf_filter* call on this plan (f and theta finite, sigma finite and > 0 --
+ * the preconditions of eq.(29), whose violation otherwise gives unspecified
+ * values).  Synchronises the plan's last stream, then writes the number of
+ * violating pixels to *bad_count and the flat index (b*H*W + y*W + x) of the
+ * first one to *first_bad (-1 if none).  The check costs one extra read of
+ * f, theta, sigma per call.  INVALID_ARGUMENT for NULL pointers or a plan
+ * made without the flag.                                                      */
+fabf_status_t fabf_debug_status(fabf_plan_t plan, long long* bad_count, long long* first_bad);
 
 /* Profiling variant of fabf_filter: same work on the same stream, with CUDA
  * events recorded between the kernels; synchronises the stream and writes the

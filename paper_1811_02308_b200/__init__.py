@@ -20,6 +20,7 @@ from .fabf import (  # noqa: F401
     version,
     FLAG_LITERAL,
     FLAG_CLAMP,
+    FLAG_DEBUG,
     CODE_IDENTITY,
     CODE_GUARD,
     CODE_SMALL_LAMBDA,

@@ -41,6 +41,8 @@ struct fabf_plan_s {
   float2* blkmm = nullptr;  // per bounds tile (min alpha, max beta)
   int* fb_count = nullptr;  // exact-moment fallback list
   int* fb_list = nullptr;
+  // FABF_FLAG_DEBUG: [0] inputs violating the preconditions, [1] the first one's index
+  unsigned long long* dbg = nullptr;
   float* h_in = nullptr;  // device staging for fabf_filter_host
   float* h_out = nullptr;
   void* last_stream = nullptr;
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 #pragma unroll
             for (int q = 0; q < N; ++q) psc[(r * NN + q) * PSQ] = V[q];
             if (WF > 0) {  // fused bounds: the ring now holds the window's WF rows
-              ring[c * WF + (Yb + r + 2 * rho - Y0) % WF] = fin[r];
+              ring[c * WF + (Yb + r + 2 * rho - Y0) % (WF > 0 ? WF : 1)] = fin[r];
               float mn = ring[c * WF], mx = mn;
 #pragma unroll
               for (int d = 1; d < WF; ++d) {
@@ -1064,6 +1066,38 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
 }
 
 // ============================================================================
+// FABF_FLAG_DEBUG: device-side check of the preconditions (include/fabf.h):
+// f, theta finite, sigma finite and > 0.  Counts violations of the pixels
+// [lo, lo + n) of each image b0 .. b0 + nb - 1 and keeps the smallest index.
+__global__ void __launch_bounds__(kThreads) k_validate(const float* __restrict__ img,
+                                                        const float* __restrict__ theta,
+                                                        const float* __restrict__ sigma, size_t plane,
+                                                        int b0, int nb, size_t lo, size_t n,
+                                                        unsigned long long* dbg) {
+  const size_t total = (size_t)nb * n;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t - threadIdx.x < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    bool bad = false;
+    unsigned long long o = ~0ull;
+    if (t < total) {
+      const size_t b = t / n;
+      o = (unsigned long long)((b0 + b) * plane + lo + (t - b * n));
+      const float f = img[o], th = theta[o], sg = sigma[o];
+      bad = !(isfinite(f) && isfinite(th) && isfinite(sg) && sg > 0.0f);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, bad);
+    if (m) {
+      unsigned long long first = bad ? o : ~0ull;
+      for (int off = 16; off > 0; off >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, off));
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&dbg[0], (unsigned long long)__popc(m));
+        atomicMin(&dbg[1], first);
+      }
+    }
+  }
+}
+
+// ============================================================================
 // host side
 namespace {
 
@@ -1309,6 +1343,12 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
                           int ty1, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int), st), "cudaMemsetAsync(fb_count)");
   p->last_stream = st;
+  if (p->flags & FABF_FLAG_DEBUG) {  // preconditions of the band's own pixels
+    const size_t lo = (size_t)ty0 * kBT * p->W, hi = (size_t)std::min(p->H, ty1 * kBT) * p->W;
+    k_validate<<<148 * 4, kThreads, 0, st>>>(img, theta, sigma, (size_t)p->H * p->W, b0, nb, lo, hi - lo,
+                                              p->dbg);
+    FABF_CUDA(cudaGetLastError(), "k_validate launch");
+  }
   // small windows: bounds inside k_filter (north_star (e): each pixel crosses
   // HBM once); the diagnostic entry point keeps the separate bounds kernel
   // because it returns the alpha / beta planes
@@ -1362,9 +1402,19 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
   return launch_filter(fa, N, nb, st);
 }
 
+// FABF_FLAG_DEBUG: a fresh status word per call (count 0, first index ~0)
+fabf_status_t debug_reset(Plan* p, cudaStream_t st) {
+  if (!(p->flags & FABF_FLAG_DEBUG)) return FABF_OK;
+  FABF_CUDA(cudaMemsetAsync(p->dbg, 0, sizeof(unsigned long long), st), "cudaMemsetAsync(dbg)");
+  FABF_CUDA(cudaMemsetAsync(p->dbg + 1, 0xff, sizeof(unsigned long long), st), "cudaMemsetAsync(dbg)");
+  return FABF_OK;
+}
+
 fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const float* sigma,
                           int rho, int N, float* out, const fabf_diag_t* diag, cudaStream_t st) {
   fabf_status_t s = validate_filter(p, img, theta, sigma, rho, N, out);
+  if (s != FABF_OK) return s;
+  s = debug_reset(p, st);
   if (s != FABF_OK) return s;
   return filter_band(p, img, theta, sigma, rho, N, out, diag, 0, p->B, 0,
                      (p->H + kBT - 1) / kBT, st);
@@ -1382,7 +1432,7 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
     return fail(FABF_ERR_INVALID_ARGUMENT, "batch, height and width must be >= 1");
   if ((size_t)batch * height * width >= (size_t)1 << 31)
     return fail(FABF_ERR_INVALID_ARGUMENT, "more than 2^31-1 pixels per call");
-  if (flags & ~(unsigned)(FABF_FLAG_LITERAL | FABF_FLAG_CLAMP))
+  if (flags & ~(unsigned)(FABF_FLAG_LITERAL | FABF_FLAG_CLAMP | FABF_FLAG_DEBUG))
     return fail(FABF_ERR_INVALID_ARGUMENT, "unknown flag bits");
   int dev = 0;
   fabf_status_t s = check_device(&dev);
@@ -1403,9 +1453,18 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
       (e = cudaMalloc(&p->blkmm, sizeof(float2) * (size_t)batch * ((height + kBT - 1) / kBT) *
                                      ((width + kBT - 1) / kBT))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_count, sizeof(int))) != cudaSuccess ||
-      (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess) {
+      (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess ||
+      ((flags & FABF_FLAG_DEBUG) &&
+       (e = cudaMalloc(&p->dbg, 2 * sizeof(unsigned long long))) != cudaSuccess)) {
     fabf_destroy(p);
     return cuda_fail(e, "cudaMalloc(plan workspace)");
+  }
+  if (p->dbg) {  // no call yet: count 0, no index
+    const unsigned long long init[2] = {0ull, ~0ull};
+    if ((e = cudaMemcpy(p->dbg, init, sizeof(init), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      fabf_destroy(p);
+      return cuda_fail(e, "cudaMemcpy(debug word)");
+    }
   }
   *plan = p;
   return FABF_OK;
@@ -1470,6 +1529,8 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   fabf_status_t s = validate_filter(p, dimg, dth, dsg, rho, N, p->h_out);
   if (s != FABF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  s = debug_reset(p, st);
+  if (s != FABF_OK) return s;
   const int H = p->H, W = p->W;
   const int ntile = (H + kBT - 1) / kBT;
   // bands of whole tiles, each at least rho + 1 rows (a band's halo then lies
@@ -1533,6 +1594,19 @@ fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count) {
   return FABF_OK;
 }
 
+fabf_status_t fabf_debug_status(fabf_plan_t plan, long long* bad_count, long long* first_bad) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  if (!p || !bad_count || !first_bad) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!(p->flags & FABF_FLAG_DEBUG)) return fail(FABF_ERR_INVALID_ARGUMENT, "plan made without FABF_FLAG_DEBUG");
+  unsigned long long w[2] = {0ull, ~0ull};
+  FABF_CUDA(cudaMemcpyAsync(w, p->dbg, sizeof(w), cudaMemcpyDeviceToHost, (cudaStream_t)p->last_stream),
+            "read debug word");
+  FABF_CUDA(cudaStreamSynchronize((cudaStream_t)p->last_stream), "cudaStreamSynchronize");
+  *bad_count = (long long)w[0];
+  *first_bad = w[0] ? (long long)w[1] : -1;
+  return FABF_OK;
+}
+
 fabf_status_t fabf_filter_profile(fabf_plan_t plan, const float* img, const float* theta,
                                   const float* sigma, int rho, int N, float* out, void* stream,
                                   float stage_ms[4]) {
@@ -1576,6 +1650,7 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   cudaFree(p->blkmm);
   cudaFree(p->fb_count);
   cudaFree(p->fb_list);
+  cudaFree(p->dbg);
   cudaFree(p->h_in);
   cudaFree(p->h_out);
   if (p->cs_in) {

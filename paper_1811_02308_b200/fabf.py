@@ -16,6 +16,7 @@ library_path = os.environ.get("FABF_LIB") or os.path.join(_PKG, "libfabf.so")  #
 
 FLAG_LITERAL = 0x1
 FLAG_CLAMP = 0x2
+FLAG_DEBUG = 0x4
 CODE_IDENTITY = 0x1
 CODE_GUARD = 0x2
 CODE_SMALL_LAMBDA = 0x4
@@ -59,10 +60,11 @@ def lib():
             L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
             L.fabf_filter_events.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_void_p)]
             L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
+            L.fabf_debug_status.argtypes = [P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
             L.fabf_destroy.argtypes = [P]
             for fn in ("fabf_plan", "fabf_filter", "fabf_filter_diag", "fabf_bounds",
                        "fabf_filter_host", "fabf_last_fallback_count", "fabf_destroy",
-                       "fabf_filter_profile", "fabf_filter_events"):
+                       "fabf_filter_profile", "fabf_filter_events", "fabf_debug_status"):
                 getattr(L, fn).restype = ctypes.c_int
             L.fabf_status_string.argtypes = [i]
             L.fabf_status_string.restype = ctypes.c_char_p
@@ -135,6 +137,12 @@ class Plan:
         c = ctypes.c_longlong(0)
         _check(lib().fabf_last_fallback_count(self._h, ctypes.byref(c)))
         return int(c.value)
+
+    def debug_status(self):
+        """FLAG_DEBUG plans: (violating pixels, first flat index or -1) of the last call."""
+        c, f = ctypes.c_longlong(0), ctypes.c_longlong(0)
+        _check(lib().fabf_debug_status(self._h, ctypes.byref(c), ctypes.byref(f)))
+        return int(c.value), int(f.value)
 
 
 def filter(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=None):

@@ -310,6 +310,38 @@ def test_fallback_modes_parity(fb, orc, tmp_path, mode, rho):
     assert nbad == 0, f"max |delta| = {mx}"
 
 
+def test_debug_flag_validates_preconditions(fb):
+    """FABF_FLAG_DEBUG: the device-side check counts pixels with sigma <= 0 or
+    a non-finite f / theta / sigma and reports the first one's flat index;
+    clean inputs report (0, -1); the host entry point checks every band; a plan
+    without the flag refuses the query."""
+    import torch
+
+    w = workloads.config(1, scale=0.5)
+    B, H, W = w.shape
+    plan = fb.Plan(B, H, W, fb.FLAG_DEBUG)
+    img, th, sg = _dev(w.img), _dev(w.theta), _dev(w.sigma)
+    out = fb.filter(plan, img, th, sg, w.rho, w.N)
+    assert plan.debug_status() == (0, -1)
+    ref = fb.filter(fb.Plan(B, H, W), img, th, sg, w.rho, w.N)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)  # the check does not change the result
+    bad = {5 * W + 7: ("sigma", 0.0), 9 * W + 1: ("theta", float("nan")),
+           (H - 1) * W + W - 1: ("sigma", -2.0), 3 * W + 100: ("img", float("inf"))}
+    planes = {"img": w.img.copy(), "theta": w.theta.copy(), "sigma": w.sigma.copy()}
+    for o, (name, v) in bad.items():
+        planes[name].reshape(-1)[o] = v
+    fb.filter(plan, _dev(planes["img"]), _dev(planes["theta"]), _dev(planes["sigma"]), w.rho, w.N)
+    assert plan.debug_status() == (len(bad), min(bad))
+    host_out = np.empty_like(w.img)
+    fb.filter_host(plan, planes["img"], planes["theta"], planes["sigma"], w.rho, w.N, host_out)
+    assert plan.debug_status() == (len(bad), min(bad))
+    fb.filter(plan, img, th, sg, w.rho, w.N)  # a fresh word per call
+    assert plan.debug_status() == (0, -1)
+    with pytest.raises(fb.FabfError):
+        fb.Plan(B, H, W).debug_status()
+
+
 def test_filter_events_matches_filter(fb):
     """fabf_filter_events: same output as fabf_filter, five recorded events in
     kernel order with non-negative gaps (no host sync inside)."""
