@@ -866,11 +866,12 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       __syncthreads();
       // ---- phase C1: window sums, flag, regime, slot in the queue, stretch
       // ---- written straight into the slot
+      // (two passes: regimes of this thread's PPT pixels first, so that one
+      // shared atomic per warp and step reserves the slots of all of them)
+      int regime[PPT];
 #pragma unroll
       for (int i = 0; i < PPT; ++i) {
-        int regime = -1;  // -1: no record (invalid, identity or fallback)
-        double S[N + 1];
-        double au = 0.0, bu = 0.0;
+        regime[i] = -1;  // -1: no record (invalid, identity or fallback)
         if (WF > 0 && pvalid[i]) {  // fused bounds: horizontal min / max of vmm
           const float2* vr = vmm + (px_r + i * (kThreads / TW)) * L + px_x;
           float2 m = vr[0];
@@ -889,46 +890,54 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             if (a.d_kappa) a.d_kappa[po[i]] = 1.0f;
             if (a.d_t2n) a.d_t2n[po[i]] = 1.0f;
             if (a.d_code) a.d_code[po[i]] = (unsigned char)kCodeIdentity;
-          } else {
-            au = fma((double)p_al[i], invS, mcs);
-            bu = fma((double)p_be[i], invS, mcs);
-            if (stretch_flagged(au, bu, a.flag_root)) {  // exact-moment fallback pass
-              const int slotfb = atomicAdd(a.fb_count, 1);
-              a.fb_list[slotfb] = po[i];
-              if (WF > 0) {  // the fallback kernel reads alpha, beta from the plan
-                a.alpha_w[po[i]] = p_al[i];
-                a.beta_w[po[i]] = p_be[i];
-              }
-            } else {
-              float lam, t0;
-              regime = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
-              S[0] = (double)n;
-              const double* prow = Ps + (px_r + i * (kThreads / TW)) * NN * PSQ + px_x;
-              if (WD == 0) {
-#pragma unroll
-                for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
-              } else {
-#pragma unroll
-                for (int q = 1; q <= N; ++q) {
-                  double acc = 0.0;
-#pragma unroll
-                  for (int d = 1; d <= WD; ++d) acc += prow[(q - 1) * PSQ + d];
-                  S[q] = acc;
-                }
-              }
+          } else if (stretch_flagged(fma((double)p_al[i], invS, mcs), fma((double)p_be[i], invS, mcs),
+                                     a.flag_root)) {  // exact-moment fallback pass
+            const int slotfb = atomicAdd(a.fb_count, 1);
+            a.fb_list[slotfb] = po[i];
+            if (WF > 0) {  // the fallback kernel reads alpha, beta from the plan
+              a.alpha_w[po[i]] = p_al[i];
+              a.beta_w[po[i]] = p_be[i];
             }
+          } else {
+            float lam, t0;
+            regime[i] = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
           }
         }
-        const unsigned mA = __ballot_sync(0xffffffffu, regime == kRegA);
-        const unsigned mB = __ballot_sync(0xffffffffu, regime > kRegA);
-        int old = 0;  // one atomic for both counters (QS <= 512 < 2^16)
-        if (lane == 0 && (mA | mB)) old = atomicAdd(&cnt[qb], __popc(mA) | (__popc(mB) << 16));
-        old = __shfl_sync(0xffffffffu, old, 0);
-        const int baseA = old & 0xffff, baseB = old >> 16;
-        const unsigned lt = (1u << lane) - 1u;
-        if (regime >= 0) {
-          const int j = (regime == kRegA) ? baseA + __popc(mA & lt)
-                                          : QS - 1 - (baseB + __popc(mB & lt));
+      }
+      unsigned mA[PPT], mB[PPT];
+      int inc = 0;
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        mA[i] = __ballot_sync(0xffffffffu, regime[i] == kRegA);
+        mB[i] = __ballot_sync(0xffffffffu, regime[i] > kRegA);
+        inc += __popc(mA[i]) | (__popc(mB[i]) << 16);
+      }
+      int old = 0;  // one atomic for both counters (QS <= 512 < 2^16) and all PPT pixels
+      if (lane == 0 && inc) old = atomicAdd(&cnt[qb], inc);
+      old = __shfl_sync(0xffffffffu, old, 0);
+      int baseA = old & 0xffff, baseB = old >> 16;
+      const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        if (regime[i] >= 0) {
+          double S[N + 1];
+          S[0] = (double)n;
+          const double* prow = Ps + (px_r + i * (kThreads / TW)) * NN * PSQ + px_x;
+          if (WD == 0) {
+#pragma unroll
+            for (int q = 1; q <= N; ++q) S[q] = prow[(q - 1) * PSQ + w] - prow[(q - 1) * PSQ];
+          } else {
+#pragma unroll
+            for (int q = 1; q <= N; ++q) {
+              double acc = 0.0;
+#pragma unroll
+              for (int d = 1; d <= WD; ++d) acc += prow[(q - 1) * PSQ + d];
+              S[q] = acc;
+            }
+          }
+          const double au = fma((double)p_al[i], invS, mcs), bu = fma((double)p_be[i], invS, mcs);
+          const int j = (regime[i] == kRegA) ? baseA + __popc(mA[i] & lt)
+                                             : QS - 1 - (baseB + __popc(mB[i] & lt));
           nu_from_sums<N>(S, au, bu, qnu + j, QS);
           qth[j] = p_th[i];
           qsg[j] = p_sg[i];
@@ -936,6 +945,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           qbe[j] = p_be[i];
           qo[j] = po[i];
         }
+        baseA += __popc(mA[i]);
+        baseB += __popc(mB[i]);
       }
       __syncthreads();
       // ---- phase C2: integrals, ratio, guard, store (one regime per warp).  No
