@@ -514,7 +514,7 @@ struct FilterGeom {
 template <int N, int E>
 struct FilterSmem {
   // byte offsets into dynamic shared memory
-  size_t ps, vs, qnu, qth, qsg, qal, qbe, qo, ring, vmm, total;
+  size_t ps, vs, qnu, q4, qo, ring, vmm, total;
   __host__ __device__ FilterSmem(int L, int RB, int QS, int WF = 0) {
     using G = FilterGeom<N, E>;
     size_t off = 0;
@@ -526,14 +526,9 @@ struct FilterSmem {
     // step s+1 and C1 of step s+1 writes it after the next one: single buffer
     qnu = off;
     off += sizeof(double) * (size_t)(N + 1) * QS;
-    qth = off;
-    off += sizeof(float) * QS;
-    qsg = off;
-    off += sizeof(float) * QS;
-    qal = off;
-    off += sizeof(float) * QS;
-    qbe = off;
-    off += sizeof(float) * QS;
+    off = (off + 15) & ~(size_t)15;
+    q4 = off;  // (theta, sigma, alpha, beta) of each record: one 16-byte access
+    off += sizeof(float4) * QS;
     qo = off;
     off += sizeof(int) * QS;
     // fused bounds (WF = 2 rho + 1 > 0): per-column ring of the last WF rows,
@@ -566,10 +561,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   double* Ps = reinterpret_cast<double*>(smraw + lay.ps);    // [RB][NN][PSQ]
   double* Vs = reinterpret_cast<double*>(smraw + lay.vs);    // [L][VST]
   double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [N+1][QS]
-  float* qth = reinterpret_cast<float*>(smraw + lay.qth);
-  float* qsg = reinterpret_cast<float*>(smraw + lay.qsg);
-  float* qal = reinterpret_cast<float*>(smraw + lay.qal);
-  float* qbe = reinterpret_cast<float*>(smraw + lay.qbe);
+  float4* q4 = reinterpret_cast<float4*>(smraw + lay.q4);
   int* qo = reinterpret_cast<int*>(smraw + lay.qo);
   const float n = (float)(w * w);
   const bool want_t2n = a.d_t2n != nullptr;
@@ -939,10 +931,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           const int j = (regime[i] == kRegA) ? baseA + __popc(mA[i] & lt)
                                              : QS - 1 - (baseB + __popc(mB[i] & lt));
           nu_from_sums<N>(S, au, bu, qnu + j, QS);
-          qth[j] = p_th[i];
-          qsg[j] = p_sg[i];
-          qal[j] = p_al[i];
-          qbe[j] = p_be[i];
+          q4[j] = make_float4(p_th[i], p_sg[i], p_al[i], p_be[i]);
           qo[j] = po[i];
         }
         baseA += __popc(mA[i]);
@@ -959,7 +948,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           if (j < nA || j >= QS - nBC) {
             const double* nu = qnu + j;  // nu[k * QS]
             const int o = qo[j];
-            const float th = qth[j], sg = qsg[j], al = qal[j], be = qbe[j];
+            const float4 rec = q4[j];
+            const float th = rec.x, sg = rec.y, al = rec.z, be = rec.w;
             int regime = kRegA;
             if (j >= nA) {
               float lam, t0;
