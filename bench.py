@@ -292,7 +292,7 @@ def run_gpu(args):
         fb.filter_host(plan, h_img, h_th, h_sg, w.rho, w.N, h_out)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 10))
+        e2e_steps = max(3, min(args.steps, 20))
         for _ in range(e2e_steps):
             fb.filter_host(plan, h_img, h_th, h_sg, w.rho, w.N, h_out)
         e2e_s = time.perf_counter() - t0
