@@ -18,9 +18,12 @@
  *   fabfo_fast     the paper's approximation g-hat of eq.(29), per
  *                  pixel, evaluated in __float128:
  *                    mu_k  = sum_{t in Gamma_i} t^k H_i(t)      eq.(22)
- *                            (the stretched moments, summed directly over the
- *                            window; Prop.3 / eq.(24) is checked against this in
- *                            tests, it is not needed to *define* mu)
+ *                            (the stretched moments, summed over the distinct
+ *                            values of the window weighted by their counts --
+ *                            the histogram h_i of eq.(5) P:184-189 -- and
+ *                            cross-checked against the sample-by-sample sum;
+ *                            Prop.3 / eq.(24) is checked against this in tests,
+ *                            it is not needed to *define* mu)
  *                    c     = A^{-1} mu, A^{-1} by Theorem 1     eq.(19)
  *                    lambda, theta_0                           eq.(25)
  *                    I_0..I_{N+1}                              eq.(28)
@@ -162,11 +165,21 @@ static qd binom_q(int n, int k) {
 
 /* Theorem 1, eq.(19) P:290-299, 1-based indices m, n = 1..N+1:                */
 /* (A^{-1})_{mn} = (-1)^{m+n} (m+n-1) C(N+m, N+1-n) C(N+n, N+1-m) C(m+n-2,m-1)^2 */
-static qd hilbert_inv_entry(int N, int m, int n) {
+static qd hilbert_inv_entry_formula(int N, int m, int n) {
   qd b3 = binom_q(m + n - 2, m - 1);
   qd v = (qd)(m + n - 1) * binom_q(N + m, N + 1 - n) * binom_q(N + n, N + 1 - m) * b3 * b3;
   return ((m + n) % 2) ? -v : v;
 }
+
+/* eq.(19)'s entries for every N <= FABFO_MAX_N, evaluated once at load time
+ * (the same exact integers, looked up instead of re-multiplied per pixel)    */
+static qd hinv_tab[FABFO_MAX_N + 1][FABFO_MAX_N + 1][FABFO_MAX_N + 1];
+__attribute__((constructor)) static void hinv_init(void) {
+  for (int N = 0; N <= FABFO_MAX_N; ++N)
+    for (int m = 1; m <= N + 1; ++m)
+      for (int n = 1; n <= N + 1; ++n) hinv_tab[N][m - 1][n - 1] = hilbert_inv_entry_formula(N, m, n);
+}
+static qd hilbert_inv_entry(int N, int m, int n) { return hinv_tab[N][m - 1][n - 1]; }
 
 int fabfo_hilbert_inverse(int N, double* out) {
   if (N < 0 || N > FABFO_MAX_N || !out) return 1;
@@ -301,9 +314,76 @@ int fabfo_integrals(double lam, double t0, int K, double* I, int method) {
 /* shifted Legendre polynomial coefficients: P~_k(t) = P_k(2t-1)
  * = sum_r (-1)^{k+r} C(k,r) C(k+r,r) t^r  (used only for the diagnostic kappa
  * of reading R7 -- the guard's condition number is stated in this basis).      */
-static qd shifted_legendre_coef(int k, int r) {
+static qd shifted_legendre_coef_formula(int k, int r) {
   qd v = binom_q(k, r) * binom_q(k + r, r);
   return ((k + r) % 2) ? -v : v;
+}
+static qd sleg_tab[FABFO_MAX_N + 1][FABFO_MAX_N + 1];
+__attribute__((constructor)) static void sleg_init(void) {
+  for (int k = 0; k <= FABFO_MAX_N; ++k)
+    for (int r = 0; r <= k; ++r) sleg_tab[k][r] = shifted_legendre_coef_formula(k, r);
+}
+static qd shifted_legendre_coef(int k, int r) { return sleg_tab[k][r]; }
+
+/* ------------------------------------------------------------------------- */
+/* eq.(22): the stretched moments mu_k = sum_{t in Gamma_i} t^k H_i(t)
+ * of the window whose samples are vals[0..n-1] (alpha, beta = their min, max).
+ * H_i is the histogram of eq.(5) P:184-189 moved to Gamma_i by eq.(20)-(21)
+ * P:301-310; with omega == 1 (reading R1) h_i(t) is the number of samples equal
+ * to t.  route 0 follows eq.(22) as printed: the distinct values t of the
+ * window with their counts (a counting table when the samples are integers
+ * spanning at most 4096 levels -- every workload image -- else a sorted copy,
+ * qsort being a library primitive); route 1 sums t_j^k over the n samples one by
+ * one (the same sum, term by term; kept as the cross-check of route 0).  Both
+ * in __float128; they differ only in the order of additions.                 */
+static int cmp_float(const void* a, const void* b) {
+  const float x = *(const float*)a, y = *(const float*)b;
+  return (x > y) - (x < y);
+}
+
+#define FABFO_HIST_SPAN 4096
+
+static void add_powers(qd t, qd count, int N, qd* mu) {
+  qd tp = count;
+  for (int k = 0; k <= N; ++k) {
+    mu[k] += tp;
+    tp *= t;
+  }
+}
+
+static void stretched_moments(const float* vals, int n, float amin, float bmax, int N, int route,
+                              qd* mu) {
+  const qd alpha = amin, d = (qd)bmax - (qd)amin;
+  for (int k = 0; k <= N; ++k) mu[k] = 0;
+  if (route == 1) {
+    for (int j = 0; j < n; ++j) add_powers(((qd)vals[j] - alpha) / d, 1, N, mu);
+    return;
+  }
+  int integral = (double)bmax - (double)amin <= FABFO_HIST_SPAN;
+  for (int j = 0; j < n && integral; ++j) integral = vals[j] == floorf(vals[j]);
+  if (integral) { /* counts of the levels amin .. bmax */
+    static __thread int cnt[FABFO_HIST_SPAN + 1];
+    const int span = (int)((double)bmax - (double)amin);
+    memset(cnt, 0, sizeof(int) * (size_t)(span + 1));
+    for (int j = 0; j < n; ++j) cnt[(int)((double)vals[j] - (double)amin)]++;
+    for (int v = 0; v <= span; ++v)
+      if (cnt[v]) add_powers((qd)v / d, (qd)cnt[v], N, mu);
+    return;
+  }
+  float* s = (float*)malloc(sizeof(float) * (size_t)n);
+  if (!s) { /* out of memory: the term-by-term sum is the same quantity */
+    for (int j = 0; j < n; ++j) add_powers(((qd)vals[j] - alpha) / d, 1, N, mu);
+    return;
+  }
+  memcpy(s, vals, sizeof(float) * (size_t)n);
+  qsort(s, (size_t)n, sizeof(float), cmp_float);
+  for (int j = 0; j < n;) {
+    int e = j + 1;
+    while (e < n && s[e] == s[j]) ++e;
+    add_powers(((qd)s[j] - alpha) / d, (qd)(e - j), N, mu);
+    j = e;
+  }
+  free(s);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -320,7 +400,7 @@ typedef struct {
 
 /* Algorithm 1 P:446-477 for one pixel whose window samples are vals[0..n-1]  */
 static void fast_window(const float* vals, int n, float f_center, float theta, float sigma,
-                        int N, fabfo_px* out) {
+                        int N, int route, fabfo_px* out) {
   memset(out, 0, sizeof(*out));
   float amin = vals[0], bmax = vals[0];
   for (int j = 1; j < n; ++j) {
@@ -336,16 +416,9 @@ static void fast_window(const float* vals, int n, float f_center, float theta, f
   }
   qd alpha = amin, beta = bmax, d = beta - alpha;
 
-  /* eq.(22): mu_k = sum_{t in Gamma_i} t^k H_i(t) = sum_j ((f_j - alpha)/d)^k */
+  /* eq.(22): mu_k = sum_{t in Gamma_i} t^k H_i(t) */
   qd mu[FABFO_MAX_N + 1];
-  for (int k = 0; k <= N; ++k) mu[k] = 0;
-  for (int j = 0; j < n; ++j) {
-    qd t = ((qd)vals[j] - alpha) / d, tp = 1;
-    for (int k = 0; k <= N; ++k) {
-      mu[k] += tp;
-      tp *= t;
-    }
-  }
+  stretched_moments(vals, n, amin, bmax, N, route, mu);
   /* line 11: c = A^{-1} mu */
   qd c[FABFO_MAX_N + 1];
   fit_q(mu, N, c);
@@ -390,12 +463,13 @@ static void fast_window(const float* vals, int n, float f_center, float theta, f
   out->code = code;
 }
 
-/* one window given explicitly: out6 = {g_lit, g_guard, kappa, t2n, lam, t0}   */
+/* one window given explicitly: out6 = {g_lit, g_guard, kappa, t2n, lam, t0};
+ * route: how eq.(22) is summed (0 distinct values with counts, 1 sample by sample) */
 int fabfo_window(const float* vals, int n, float f_center, float theta, float sigma, int N,
-                 double* out6, int* code) {
-  if (!vals || n < 1 || N < 0 || N > FABFO_MAX_N || !out6) return 1;
+                 int route, double* out6, int* code) {
+  if (!vals || n < 1 || N < 0 || N > FABFO_MAX_N || !out6 || route < 0 || route > 1) return 1;
   fabfo_px px;
-  fast_window(vals, n, f_center, theta, sigma, N, &px);
+  fast_window(vals, n, f_center, theta, sigma, N, route, &px);
   out6[0] = px.g_lit;
   out6[1] = px.g_guard;
   out6[2] = px.kappa;
@@ -427,7 +501,7 @@ int fabfo_fast(const float* img, const float* theta, const float* sigma, int B, 
     long b = p / HW, r = p % HW, y = r / W, x = r % W;
     gather_window(img, H, W, rho, b, y, x, vals);
     fabfo_px px;
-    fast_window(vals, n, img[p], theta[p], sigma[p], N, &px);
+    fast_window(vals, n, img[p], theta[p], sigma[p], N, 0, &px);
     if (g_lit) g_lit[q] = px.g_lit;
     if (g_guard) g_guard[q] = px.g_guard;
     if (kappa) kappa[q] = px.kappa;

@@ -49,7 +49,7 @@ def _load():
             lib.fabfo_bounds.argtypes = [P, i, i, i, i, l, l, P, P]
             lib.fabfo_brute.argtypes = [P, P, P, i, i, i, i, l, l, P]
             lib.fabfo_fast.argtypes = [P, P, P, i, i, i, i, i, P, l, l, P, P, P, P, P]
-            lib.fabfo_window.argtypes = [P, i, ctypes.c_float, ctypes.c_float, ctypes.c_float, i, P, P]
+            lib.fabfo_window.argtypes = [P, i, ctypes.c_float, ctypes.c_float, ctypes.c_float, i, i, P, P]
             lib.fabfo_hilbert_inverse.argtypes = [i, P]
             lib.fabfo_fit.argtypes = [P, i, P]
             lib.fabfo_stretch.argtypes = [P, i, d, d, P]
@@ -162,13 +162,17 @@ def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None =
     return out
 
 
-def fast_window(vals, f_center: float, theta: float, sigma: float, N: int):
-    """g-hat for one explicit window (samples ``vals``): dict of scalars."""
+def fast_window(vals, f_center: float, theta: float, sigma: float, N: int, route: int = 0):
+    """g-hat for one explicit window (samples ``vals``): dict of scalars.
+
+    ``route`` selects how eq.(22) is summed: 0 over the window's distinct values
+    weighted by their counts (the histogram of eq.(5); what ``fast`` uses), 1
+    sample by sample."""
     lib = _load()
     v = _f32(vals).ravel()
     o = np.empty(6, np.float64)
     code = ctypes.c_int(0)
-    if lib.fabfo_window(_ptr(v), v.size, float(f_center), float(theta), float(sigma), N, _ptr(o),
+    if lib.fabfo_window(_ptr(v), v.size, float(f_center), float(theta), float(sigma), N, int(route), _ptr(o),
                         ctypes.byref(code)):
         raise ValueError("fabfo_window: invalid arguments")
     return dict(g_lit=o[0], g_guard=o[1], kappa=o[2], t2n=o[3], lam=o[4], t0=o[5], code=code.value)

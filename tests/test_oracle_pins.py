@@ -384,3 +384,27 @@ def test_psnr_trend_with_N(orc):
         mse = np.mean((o["g_guard"] - g) ** 2)
         ps.append(10 * np.log10(255 ** 2 / mse))
     assert ps[0] < ps[1] < ps[2] and ps[2] > 40.0
+
+
+@pytest.mark.parametrize("kind", ["integer", "float", "wide_integer"])
+def test_histogram_route_equals_sample_sums(orc, kind):
+    """eq.(22) summed over the distinct values t of the window weighted by the
+    histogram H_i(t) of eq.(5)/(21) (the oracle's route) equals the same sum taken
+    sample by sample: the two differ only in the order of __float128 additions."""
+    rng = np.random.default_rng({"integer": 1, "float": 2, "wide_integer": 3}[kind])
+    for trial in range(40):
+        n = int(rng.choice([9, 49, 121, 1681]))
+        if kind == "integer":  # the workloads: 0..255 levels, many repeats
+            vals = np.rint(np.clip(rng.normal(120, 25, n), 0, 255)).astype(np.float32)
+        elif kind == "float":  # non-integer: the sorted-copy route
+            vals = rng.normal(0.3, 2.0, n).astype(np.float32)
+            vals[: n // 3] = vals[0]  # repeated values too
+        else:  # integers spanning more than the counting table: sorted route
+            vals = rng.integers(-30000, 30000, n).astype(np.float32)
+        N = int(rng.integers(0, 11))
+        theta = float(vals.mean() + rng.normal(0, 5))
+        sigma = float(rng.uniform(2, 60))
+        a = orc.fast_window(vals, vals[n // 2], theta, sigma, N, route=0)
+        b = orc.fast_window(vals, vals[n // 2], theta, sigma, N, route=1)
+        for k in ("g_lit", "g_guard", "kappa", "t2n"):
+            assert a[k] == pytest.approx(b[k], rel=1e-13, abs=1e-13), (trial, k)
