@@ -109,30 +109,57 @@ class ClockSampler:
 # B200 FP64 pipe: 64 FMA/clk/SM (microbench: 1.71e13 FMA/s at the clocks seen,
 # profiles/r1_microbench.json) x 148 SMs x 1.965 GHz max clock x 2 flop/FMA.
 FP64_PEAK_TFLOPS = 64 * 148 * 1.965e9 * 2 / 1e12  # 37.2, derived from unit counts and clocks
+FP64_MICROBENCH_TFLOPS = 34.19  # tools/microbench.cu, profiles/r1_microbench.json
+FP64_PEAK_SOURCE = ("derived from unit counts and clocks: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz x 2 "
+                    "= 37.2 TF/s (not driver-measured; tools/microbench.cu measured 34.2 TF/s)")
+J_STAGE_FP64 = 200  # fp64 J-stage (seeds + recurrence) of a lambda >= 2 pixel, ~170-230
 
 
-def fp64_flops_per_pixel(N: int) -> int:
-    """Algorithmic fp64 flops per pixel of the dominant kernel k_filter (FMA = 2),
-    counted from the method's steps as implemented (DESIGN.md section 4,
-    'Roofline'); halo columns, prologue rows and the fp32 small-lambda regime
-    are NOT counted (every pixel is charged the regime-A recipe).
-      a3 moments : u of the entering / leaving sample 2*2, powers 2(N-1),
-                   vertical add/sub 2N, prefix add N, window difference N
-      a4 stretch : m, h 4; Taylor shift N(N+1)/2 FMA; scaling 2N-1;
-                   Legendre sum_k (k//2+1) FMA
-      a7 seeds   : range parameters 2 rcp (MUFU + 2 Newton = 4 FMA) + 10;
-                   2 erfcx (rcp 4 FMA, 2 FMA, degree-20 Horner, 1 mul);
-                   2 exp (shifter FMA + add, 2 FMA reduction, degree-12 Horner, 1 mul);
-                   erf combination 8
-      a7 recurrence: per k <= N: X_k 2 FMA, A_{k+1} FMA + mul, D update FMA
-      a8 contraction: per k <= N: 3 FMA (T2, U, |.| sum)
-    """
-    a3 = 2 * 2 + 2 * (N - 1) + 2 * N + N + N
-    a4 = 4 + 2 * (N * (N + 1) // 2) + (2 * N - 1) + 2 * sum(k // 2 + 1 for k in range(N + 1))
-    seeds = 2 * (2 * 4) + 10 + 2 * (2 * 4 + 2 * 2 + 2 * 20 + 1) + 2 * (2 + 1 + 2 * 2 + 2 * 12 + 1) + 8
-    rec = (N + 1) * (2 * 2 + 3 + 2)
-    con = (N + 1) * 3 * 2
-    return a3 + a4 + seeds + rec + con
+def alg_fp64_flops_per_pixel(N: int, share_fp64_j: float, share_identity: float = 0.0) -> float:
+    """ALGORITHMIC fp64 flops per pixel: moments 6N, stretch +
+    Legendre 1.5N^2 + 3.5N, and the fp64 J-stage (~200) only for the share of
+    pixels that need it (lambda >= 2 or theta far outside [alpha, beta]; the
+    lambda < 2 pixels use fp32 quadrature, no fp64); identity pixels (alpha ==
+    beta) do no per-pixel work.  The share comes from one diagnostic call
+    outside the timed region (regime codes, fabf_filter_diag)."""
+    per = 6 * N + 1.5 * N * N + 3.5 * N
+    return (1.0 - share_identity) * per + share_fp64_j * J_STAGE_FP64
+
+
+def _ncu_summary(kernel: str):
+    """Executed-pipe figures of ``kernel`` from the committed ncu --set full
+    summary (profiles/ncu_summary.json, written by tools/ncu_summary.py), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(kernel, {})
+    except Exception:
+        return {}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def regime_mix(fb, plan, img, th, sg, rho, N):
+    """Shares of identity, small-lambda (fp32 J) and fp64-J pixels, from the
+    per-pixel codes of one fabf_filter_diag call (outside any timed region)."""
+    import torch
+
+    _, d = fb.filter_diag(plan, img, th, sg, rho, N)
+    code = d["code"]
+    n = code.numel()
+    ident = int(((code & fb.CODE_IDENTITY) > 0).sum())
+    small = int(((code & fb.CODE_SMALL_LAMBDA) > 0).sum())
+    torch.cuda.synchronize()
+    return {"identity": ident / n, "small_lambda_fp32": small / n,
+            "fp64_j": (n - ident - small) / n}
 
 
 def _traffic(kernel: str):
@@ -253,6 +280,7 @@ def run_gpu(args):
         flush.fill_(float(i))
         fb.filter_events(plan, img, th, sg, w.rho, w.N, wev, out=out)
     torch.cuda.synchronize()
+    launches_per_step = plan.last_launch_count()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     # five CUDA events per step around the step's kernels (fabf_filter_events,
@@ -281,6 +309,8 @@ def run_gpu(args):
     tot_ms = float(sum(step_ms))
     fallback = plan.last_fallback_count()
     clk.__exit__(None, None, None)
+    mix = regime_mix(fb, plan, img, th, sg, w.rho, w.N)  # outside the timed region
+    others = {} if args.no_other_configs else other_configs(fb, dev, flush)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
     e2e_steps, e2e_s = 0, 0.0
@@ -312,13 +342,22 @@ def run_gpu(args):
                "unit": "GB/s", "frac": alg_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                "traffic": None, "peak_source": peak_src, "scope": "whole step, 16 B/px"}
         kf_ms = float(stage[2])  # dominant kernel k_filter, CUDA events on the launch stream
-        flops = fp64_flops_per_pixel(w.N) * px
-        fp64 = {"bound": "alu", "pipe": "fp64", "achieved": flops / (kf_ms * 1e-3) / 1e12,
-                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": flops / (kf_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                "traffic": _traffic("k_filter"), "kernel": "k_filter", "kernel_ms": kf_ms,
-                "kernel_share_of_step": kf_ms / ms,
-                "flops_per_pixel": fp64_flops_per_pixel(w.N),
-                "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz x 2 (microbench measured 34.2 TF/s)"}
+        fpp = alg_fp64_flops_per_pixel(w.N, mix["fp64_j"], mix["identity"])
+        flops = fpp * px
+        ach = flops / (kf_ms * 1e-3) / 1e12
+        nc = _ncu_summary("k_filter")
+        fp64 = {"bound": "alu", "pipe": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": _traffic("k_filter"), "kernel": "k_filter",
+                "kernel_ms": kf_ms, "kernel_share_of_step": kf_ms / ms,
+                "alg_flops_per_pixel": fpp,
+                "alg_flops_recipe": "SURVEY.md 8(d): 6N moments + 1.5N^2+3.5N stretch + 200 fp64 J-stage "
+                                    "on the fp64-J share of pixels",
+                "regime_mix": mix,
+                "peak_source": FP64_PEAK_SOURCE,
+                "frac_of_microbench_peak": ach / FP64_MICROBENCH_TFLOPS,
+                "executed_fp64_pipe_util_ncu": nc.get("fp64_pipe_pct"),
+                "issue_active_ncu": nc.get("issue_active_pct"),
+                "ncu_source": nc.get("source")}
         line = {
             "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -335,7 +374,9 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": "Mpix/s", "h2d_bytes_per_step": 12 * px,
                     "d2h_bytes_per_step": 4 * px,
                     "path": "fabf_filter_host: pinned host buffers, row-band pipelined H2D / kernels / D2H"},
-            "gpu_launches": 3 * args.steps,  # k_bounds, k_filter, k_fallback per step
+            "gpu_launches": launches_per_step * args.steps,  # fabf_last_launch_count x steps
+            "launches_per_step": launches_per_step,
+            "other_configs": others,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
@@ -343,12 +384,48 @@ def run_gpu(args):
             npx = args.ref_pixels or oracle_sample_size(w, args.ref_seconds)
             v, dt = time_oracle(w, npx)
             line["cpu_baseline"] = {"value": v, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+                                    "cpu_model": _cpu_model(),
                                     "sample": f"{npx} seeded pixels of {w.name} ({dt:.1f} s, "
                                               "__float128 Algorithm 1, all host threads)"}
+        line["paper_context"] = PAPER_CONTEXT
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+PAPER_CONTEXT = ("context only, not a target: the paper's MATLAB 9.1 implementation on a 3.4 GHz CPU "
+                 "(P:540) takes 171-189 ms for a 512x512 image at N=5 (1.4-1.5 Mpix/s) against 3.9-12.4 s "
+                 "for brute force (Table II, P:574-577): 'at least 20x' (P:90, P:564)")
+
+
+def other_configs(fb, dev, flush, steps: int = 10):
+    """Device-timed Mpix/s of BASELINE configs 1-3 (full size, L2 flushed
+    between steps, CUDA events) -- reported beside the headline config."""
+    import torch
+
+    import workloads
+
+    res = {}
+    stream = torch.cuda.current_stream()
+    for cfg in (1, 2, 3):
+        w = workloads.config(cfg)
+        img, th, sg = (torch.from_numpy(a).to(dev) for a in (w.img, w.theta, w.sigma))
+        out = torch.empty_like(img)
+        plan = fb.Plan(*w.shape)
+        for _ in range(3):
+            fb.filter(plan, img, th, sg, w.rho, w.N, out=out)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in ev:
+            flush.fill_(1.0)
+            a.record(stream)
+            fb.filter(plan, img, th, sg, w.rho, w.N, out=out)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        res[w.name] = {"Mpix/s": w.img.size / (ms * 1e-3) / 1e6, "ms": ms, "rho": w.rho, "N": w.N,
+                       "launches": plan.last_launch_count()}
+    return res
 
 
 def run_sweep(args):
@@ -385,13 +462,15 @@ def run_sweep(args):
                 stage /= args.steps
                 ms = float(stage.sum())
                 kf = float(stage[2])
-                fl = fp64_flops_per_pixel(N) * px / (kf * 1e-3) / 1e12
+                mix = regime_mix(fb, plan, img, th, sg, rho, N)
+                fl = alg_fp64_flops_per_pixel(N, mix["fp64_j"], mix["identity"]) * px / (kf * 1e-3) / 1e12
                 print(json.dumps({"sweep": "config5", "generator": gen, "rho": rho, "N": N,
                                   "images": 32, "size": 1024, "value": px / (ms * 1e-3) / 1e6,
                                   "unit": "Mpix/s", "ms_per_step": ms,
                                   "stage_ms": {"k_bounds": stage[0] + stage[1], "k_filter": kf,
                                                "k_fallback": stage[3]},
                                   "fallback_pixels": plan.last_fallback_count(),
+                                  "regime_mix": mix,
                                   "roofline": {"bound": "alu", "pipe": "fp64", "achieved": fl,
                                                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                                                "frac": fl / FP64_PEAK_TFLOPS}}), flush=True)
@@ -410,6 +489,7 @@ def main():
     ap.add_argument("--sweep-generators", default="texture,rectangles")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer pass (launch-list captures)")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the configs 1-3 throughput lines")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -127,6 +127,12 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
  * exact-moment fallback (synchronises the plan's stream to read it).         */
 fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count);
 
+/* Number of kernels the last fabf_filter / fabf_filter_diag / fabf_filter_host
+ * / fabf_filter_events / fabf_filter_profile call on this plan launched (all
+ * bands of a host call; set when the call returns, no synchronisation).
+ * INVALID_ARGUMENT for NULL pointers.                                         */
+fabf_status_t fabf_last_launch_count(fabf_plan_t plan, int* count);
+
 /* FABF_FLAG_DEBUG plans only: the device-side precondition check of the last
  * fabf_filter* call on this plan (f and theta finite, sigma finite and > 0 --
  * the preconditions of eq.(29), whose violation otherwise gives unspecified

@@ -39,8 +39,14 @@ struct fabf_plan_s {
   float* alpha = nullptr;  // workspace: bounds
   float* beta = nullptr;
   float2* blkmm = nullptr;  // per bounds tile (min alpha, max beta)
-  int* fb_count = nullptr;  // exact-moment fallback list
+  // exact-moment fallback: one counter per band of a call (slot b * kMaxBandsPlan
+  // + k for band k of image b in fabf_filter_host, slot 0 otherwise); a band's
+  // list is the region of fb_list at its own first pixel, so bands never share
+  // entries and the call's total is the sum of its slots
+  int* fb_count = nullptr;
   int* fb_list = nullptr;
+  int fb_slots = 0;  // slots the last call used
+  int launches = 0;  // kernels the last call launched (fabf_last_launch_count)
   // FABF_FLAG_DEBUG: [0] inputs violating the preconditions, [1] the first one's index
   unsigned long long* dbg = nullptr;
   float* h_in = nullptr;  // device staging for fabf_filter_host
@@ -81,6 +87,7 @@ constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // opt-in limit minus static sha
 using Plan = fabf_plan_s;
 
 thread_local std::string g_last_error;
+thread_local int g_launches = 0;  // kernels launched by the current entry point
 
 fabf_status_t fail(fabf_status_t s, const std::string& msg) {
   g_last_error = msg;
@@ -100,8 +107,10 @@ fabf_status_t cuda_fail(cudaError_t e, const char* what) {
 
 // ----------------------------------------------------------------------------
 // constant tables (computed on the host, copied once per device)
+constexpr int kMaxDevices = 64;
 std::mutex g_tables_mu;
-bool g_tables_ready[64] = {};
+bool g_tables_ready[kMaxDevices] = {};
+std::mutex g_launch_mu;  // per-device launch caches (attributes, occupancy, TMA encoder)
 
 void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
   // nodes/weights on [0,1] by Newton iteration on P_n (long double)
@@ -136,7 +145,7 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
 
 fabf_status_t ensure_tables(int dev) {
   std::lock_guard<std::mutex> lk(g_tables_mu);
-  if (dev >= 0 && dev < 64 && g_tables_ready[dev]) return FABF_OK;
+  if (g_tables_ready[dev]) return FABF_OK;
   std::vector<double> xb, wb, xc, wc;
   gauss_legendre(kGlB, xb, wb);
   gauss_legendre(kGlC, xc, wc);
@@ -157,7 +166,7 @@ fabf_status_t ensure_tables(int dev) {
   FABF_CUDA(cudaMemcpyToSymbol(c_glB_W, bW, sizeof(bW)), "cudaMemcpyToSymbol(c_glB_W)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glC_x, xc.data(), sizeof(double) * kGlC), "cudaMemcpyToSymbol(c_glC_x)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glC_w, wc.data(), sizeof(double) * kGlC), "cudaMemcpyToSymbol(c_glC_w)");
-  if (dev >= 0 && dev < 64) g_tables_ready[dev] = true;
+  g_tables_ready[dev] = true;
   return FABF_OK;
 }
 
@@ -604,11 +613,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
     if (WF > 0) {
       // fused bounds: no bounds tiles -- the range of the segment's input
-      // footprint (rows Y0-rho-1 .. Y1+rho-1 of this thread's column)
+      // footprint (rows Y0-rho .. Y1+rho-1 of this thread's column)
       if (tid < L) {
         const float* cp = a.img + plane + reflect_index(min(x0 - rho + tid, W - 1 + rho), W);
 #pragma unroll 4
-        for (int y = Y0 - rho - 1; y < Y1 + rho; ++y) {
+        for (int y = Y0 - rho; y < Y1 + rho; ++y) {
           const float v = __ldg(cp + reflect_index(y, H) * W);
           lmin = fminf(lmin, v);
           lmax = fmaxf(lmax, v);
@@ -654,7 +663,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 
     const float* colp = a.img + plane + reflect_index(min(x0 - rho + c, W - 1 + rho), W);
 
-    // prologue: rows Y0-rho-1 .. Y0+rho-1 (the first step removes Y0-rho-1)
+    // prologue: rows Y0-rho .. Y0+rho-1.  Row Y0-rho-1 lies outside every
+    // window of the segment and so possibly far outside its centring range:
+    // it is never added, and the first step's leaving sample is u = 0 (adding
+    // and then removing an outlier's powers would wipe out the fp64 sums).
     if (owner) {
       double V[NN];
 #pragma unroll
@@ -662,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // rows in batches of 8 loads issued ahead of the arithmetic (the loop is
       // otherwise one exposed L2 latency per row)
       constexpr int PB = 8;
-      for (int y0 = Y0 - rho - 1; y0 < Y0 + rho; y0 += PB) {
+      for (int y0 = Y0 - rho; y0 < Y0 + rho; y0 += PB) {
         float fb[PB];
 #pragma unroll
         for (int k = 0; k < PB; ++k) {
@@ -743,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         for (int r = 0; r < RB; ++r) {
           if (r < nr) {
             const double ui = fma((double)fin[r], invS, mcs);
-            const double uo = fma((double)fout[r], invS, mcs);
+            const double uo = (Yb + r == Y0) ? 0.0 : fma((double)fout[r], invS, mcs);
             // d_q = ui^q - uo^q by its own recurrence d_{q+1} = (ui + uo) d_q
             // - ui uo d_{q-1} (d_0 = 0): one DMUL + one DFMA per power instead
             // of two DMULs and a DADD
@@ -1115,6 +1127,7 @@ fabf_status_t check_device(int* dev_out) {
   FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   cudaDeviceProp prop;
   FABF_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+  if (dev < 0 || dev >= kMaxDevices) return fail(FABF_ERR_UNSUPPORTED, "device ordinal >= 64");
   if (prop.major != 10 || prop.minor != 0)
     return fail(FABF_ERR_UNSUPPORTED, "device is sm_" + std::to_string(prop.major) +
                                           std::to_string(prop.minor) +
@@ -1135,15 +1148,18 @@ fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha,
                                int b0, int nb, int ty0, int ty1, cudaStream_t st) {
   const bool stage = bounds_smem<RC>(rho, true) <= (size_t)kMaxDynSmem;
   const size_t smem = bounds_smem<RC>(rho, stage);
-  static bool attr_set = false;
-  if (!attr_set) {
-    FABF_CUDA(cudaFuncSetAttribute(k_bounds<RC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxDynSmem),
-              "cudaFuncSetAttribute(k_bounds)");
-    FABF_CUDA(cudaFuncSetAttribute(k_bounds<RC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxDynSmem),
-              "cudaFuncSetAttribute(k_bounds)");
-    attr_set = true;
+  {  // the dynamic-shared-memory opt-in is a per-device function attribute
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[p->device]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_bounds<RC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMaxDynSmem),
+                "cudaFuncSetAttribute(k_bounds)");
+      FABF_CUDA(cudaFuncSetAttribute(k_bounds<RC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMaxDynSmem),
+                "cudaFuncSetAttribute(k_bounds)");
+      attr_set[p->device] = true;
+    }
   }
   // TMA descriptor for interior tiles (needs 16-byte row pitch); encoded
   // once per (image pointer, rho class) through the runtime's driver entry point
@@ -1152,6 +1168,7 @@ fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha,
     p->tmap_rc = RC;
     p->tmap_ok = false;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    std::lock_guard<std::mutex> lk(g_launch_mu);
     if (!encode) {
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q;
@@ -1181,6 +1198,7 @@ fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha,
   else
     k_bounds<RC, false><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0,
                                                    ty0, p->tmap, 0);
+  ++g_launches;
   FABF_CUDA(cudaGetLastError(), "k_bounds launch");
   return FABF_OK;
 }
@@ -1226,11 +1244,11 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   const int L = TW + 2 * fa.rho, QS = PPT * kThreads, RB = QS / TW;
   const size_t smem = FilterSmem<N, E>(L, RB, QS, WF).total;
   if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
-  static int grid_cache[64] = {};  // resident CTAs per device (persistent schedule)
-  static size_t smem_cache[64] = {};
+  static int grid_cache[kMaxDevices] = {};  // resident CTAs per device (persistent schedule)
+  static size_t smem_cache[kMaxDevices] = {};
   int dev = 0;
   FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-  if (dev < 0 || dev >= 64) dev = 0;
+  std::unique_lock<std::mutex> lk(g_launch_mu);
   if (grid_cache[dev] == 0 || smem_cache[dev] != smem) {
     FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT, WD, WF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxDynSmem),
@@ -1244,7 +1262,9 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   }
   const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * (fa.r1 - fa.r0);
   const int grid = (int)std::min<long long>(grid_cache[dev], strips);
+  lk.unlock();
   k_filter<N, E, TW, PPT, WD, WF><<<grid, kThreads, smem, st>>>(fa);
+  ++g_launches;
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
   return FABF_OK;
 }
@@ -1288,6 +1308,7 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   prof_mark(3, st);
   // one thread per pixel (neighbouring list entries share their windows in L1)
   k_fallback<N><<<148 * 4, kThreads, 0, st>>>(fa, g_fb_mode);
+  ++g_launches;
   FABF_CUDA(cudaGetLastError(), "k_fallback launch");
   prof_mark(4, st);
   return FABF_OK;
@@ -1310,8 +1331,23 @@ fabf_status_t launch_filter(FilterArgs& fa, int N, int B, cudaStream_t st) {
   }
 }
 
+// a plan's workspace lives on the device it was made on; calls must be made
+// with that device current (the library never switches the caller's device)
+fabf_status_t check_plan_device(Plan* p) {
+  int dev = -1;
+  FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev != p->device)
+    return fail(FABF_ERR_INVALID_ARGUMENT, "plan was made on device " + std::to_string(p->device) +
+                                               " but device " + std::to_string(dev) + " is current");
+  return FABF_OK;
+}
+
 fabf_status_t validate_common(Plan* p, int rho) {
   if (!p) return fail(FABF_ERR_INVALID_ARGUMENT, "plan is NULL");
+  {
+    fabf_status_t s = check_plan_device(p);
+    if (s != FABF_OK) return s;
+  }
   if (rho < 0) return fail(FABF_ERR_INVALID_ARGUMENT, "rho < 0");
   if (2 * rho + 1 > p->H || 2 * rho + 1 > p->W)
     return fail(FABF_ERR_INVALID_ARGUMENT, "2*rho+1 exceeds min(height, width)");
@@ -1341,13 +1377,13 @@ fabf_status_t validate_filter(Plan* p, const float* img, const float* theta, con
 // in place); writes out, alpha, beta of the band only.
 fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const float* sigma, int rho,
                           int N, float* out, const fabf_diag_t* diag, int b0, int nb, int ty0,
-                          int ty1, cudaStream_t st) {
-  FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int), st), "cudaMemsetAsync(fb_count)");
+                          int ty1, int fb_slot, cudaStream_t st) {
   p->last_stream = st;
   if (p->flags & FABF_FLAG_DEBUG) {  // preconditions of the band's own pixels
     const size_t lo = (size_t)ty0 * kBT * p->W, hi = (size_t)std::min(p->H, ty1 * kBT) * p->W;
     k_validate<<<148 * 4, kThreads, 0, st>>>(img, theta, sigma, (size_t)p->H * p->W, b0, nb, lo, hi - lo,
                                               p->dbg);
+    ++g_launches;
     FABF_CUDA(cudaGetLastError(), "k_validate launch");
   }
   // small windows: bounds inside k_filter (north_star (e): each pixel crosses
@@ -1395,8 +1431,8 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
     const double bits = (double)kFlagBits - std::log2(mag);
     fa.flag_root = N > 0 ? std::pow(2.0, bits / N) : 1e300;
   }
-  fa.fb_count = p->fb_count;
-  fa.fb_list = p->fb_list;
+  fa.fb_count = p->fb_count + fb_slot;
+  fa.fb_list = p->fb_list + ((size_t)b0 * p->H + fa.r0) * p->W;
   fa.d_kappa = diag ? diag->kappa : nullptr;
   fa.d_t2n = diag ? diag->t2n : nullptr;
   fa.d_code = diag ? diag->code : nullptr;
@@ -1411,14 +1447,28 @@ fabf_status_t debug_reset(Plan* p, cudaStream_t st) {
   return FABF_OK;
 }
 
+// a fresh set of fallback counters per call
+fabf_status_t fallback_reset(Plan* p, int slots, cudaStream_t st) {
+  FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int) * (size_t)slots, st), "cudaMemsetAsync(fb_count)");
+  p->fb_slots = slots;
+  return FABF_OK;
+}
+
 fabf_status_t filter_impl(Plan* p, const float* img, const float* theta, const float* sigma,
                           int rho, int N, float* out, const fabf_diag_t* diag, cudaStream_t st) {
   fabf_status_t s = validate_filter(p, img, theta, sigma, rho, N, out);
   if (s != FABF_OK) return s;
+  g_launches = 0;
+  struct Record {
+    Plan* p;
+    ~Record() { p->launches = g_launches; }
+  } rec{p};
   s = debug_reset(p, st);
   if (s != FABF_OK) return s;
+  s = fallback_reset(p, 1, st);
+  if (s != FABF_OK) return s;
   return filter_band(p, img, theta, sigma, rho, N, out, diag, 0, p->B, 0,
-                     (p->H + kBT - 1) / kBT, st);
+                     (p->H + kBT - 1) / kBT, 0, st);
 }
 
 }  // namespace
@@ -1453,7 +1503,7 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
       (e = cudaMalloc(&p->beta, px * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&p->blkmm, sizeof(float2) * (size_t)batch * ((height + kBT - 1) / kBT) *
                                      ((width + kBT - 1) / kBT))) != cudaSuccess ||
-      (e = cudaMalloc(&p->fb_count, sizeof(int))) != cudaSuccess ||
+      (e = cudaMalloc(&p->fb_count, sizeof(int) * (size_t)batch * Plan::kMaxBandsPlan)) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess ||
       ((flags & FABF_FLAG_DEBUG) &&
        (e = cudaMalloc(&p->dbg, 2 * sizeof(unsigned long long))) != cudaSuccess)) {
@@ -1510,6 +1560,10 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p) return fail(FABF_ERR_INVALID_ARGUMENT, "plan is NULL");
   if (!img || !theta || !sigma || !out) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  {
+    fabf_status_t s0 = check_plan_device(p);
+    if (s0 != FABF_OK) return s0;
+  }
   const size_t px = (size_t)p->B * p->H * p->W, bytes = px * sizeof(float);
   if (!p->h_in) {
     cudaError_t e;
@@ -1524,6 +1578,11 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
       FABF_CUDA(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming), "cudaEventCreate");
     }
   }
+  g_launches = 0;
+  struct Record {
+    Plan* p;
+    ~Record() { p->launches = g_launches; }
+  } rec{p};
   float* dimg = p->h_in;
   float* dth = p->h_in + px;
   float* dsg = p->h_in + 2 * px;
@@ -1531,6 +1590,8 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   if (s != FABF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   s = debug_reset(p, st);
+  if (s != FABF_OK) return s;
+  s = fallback_reset(p, p->B * kMaxBands, st);
   if (s != FABF_OK) return s;
   const int H = p->H, W = p->W;
   const int ntile = (H + kBT - 1) / kBT;
@@ -1571,7 +1632,8 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
       FABF_CUDA(cudaMemcpyAsync(dsg + o, sigma + o, nbytes, cudaMemcpyHostToDevice, p->cs_in), "H2D sigma");
       FABF_CUDA(cudaEventRecord(p->ev_in[k], p->cs_in), "cudaEventRecord");
       FABF_CUDA(cudaStreamWaitEvent(st, p->ev_in[k], 0), "cudaStreamWaitEvent");
-      s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[k], tb[k + 1], st);
+      s = filter_band(p, dimg, dth, dsg, rho, N, p->h_out, nullptr, b, 1, tb[k], tb[k + 1], b * kMaxBands + k,
+                      st);
       if (s != FABF_OK) return s;
       FABF_CUDA(cudaEventRecord(p->ev_done[k], st), "cudaEventRecord");
       FABF_CUDA(cudaStreamWaitEvent(p->cs_out, p->ev_done[k], 0), "cudaStreamWaitEvent");
@@ -1586,12 +1648,23 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
 fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p || !count) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
-  int c = 0;
-  FABF_CUDA(cudaMemcpyAsync(&c, p->fb_count, sizeof(int), cudaMemcpyDeviceToHost,
-                            (cudaStream_t)p->last_stream),
-            "read fallback count");
-  FABF_CUDA(cudaStreamSynchronize((cudaStream_t)p->last_stream), "cudaStreamSynchronize");
-  *count = c;
+  std::vector<int> c((size_t)std::max(1, p->fb_slots), 0);
+  if (p->fb_slots > 0) {
+    FABF_CUDA(cudaMemcpyAsync(c.data(), p->fb_count, sizeof(int) * (size_t)p->fb_slots, cudaMemcpyDeviceToHost,
+                              (cudaStream_t)p->last_stream),
+              "read fallback count");
+    FABF_CUDA(cudaStreamSynchronize((cudaStream_t)p->last_stream), "cudaStreamSynchronize");
+  }
+  long long total = 0;
+  for (int v : c) total += v;
+  *count = total;
+  return FABF_OK;
+}
+
+fabf_status_t fabf_last_launch_count(fabf_plan_t plan, int* count) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  if (!p || !count) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  *count = p->launches;
   return FABF_OK;
 }
 

@@ -60,10 +60,11 @@ def lib():
             L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
             L.fabf_filter_events.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_void_p)]
             L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
+            L.fabf_last_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
             L.fabf_debug_status.argtypes = [P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
             L.fabf_destroy.argtypes = [P]
             for fn in ("fabf_plan", "fabf_filter", "fabf_filter_diag", "fabf_bounds",
-                       "fabf_filter_host", "fabf_last_fallback_count", "fabf_destroy",
+                       "fabf_filter_host", "fabf_last_fallback_count", "fabf_last_launch_count", "fabf_destroy",
                        "fabf_filter_profile", "fabf_filter_events", "fabf_debug_status"):
                 getattr(L, fn).restype = ctypes.c_int
             L.fabf_status_string.argtypes = [i]
@@ -85,14 +86,42 @@ def _check(status: int):
         raise FabfError(status, lib().fabf_last_error_message().decode())
 
 
-def _dev_ptr(t, name):
+def _numel(shape):
+    return shape[0] * shape[1] * shape[2]
+
+
+def _dev_ptr(t, name, plan=None):
+    """Device pointer of a contiguous float32 CUDA tensor holding exactly the
+    plan's batch*height*width pixels (the C ABI reads and writes that many)."""
     import torch
 
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise FabfError(1, f"{name} must be a CUDA tensor")
     if t.dtype != torch.float32 or not t.is_contiguous():
         raise FabfError(1, f"{name} must be contiguous float32")
+    if plan is not None and t.numel() != _numel(plan.shape):
+        raise FabfError(1, f"{name} has {t.numel()} elements, the plan {plan.shape} needs {_numel(plan.shape)}")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_ptr(a, name, plan):
+    """Host pointer of a contiguous float32 numpy array or CPU tensor with the
+    plan's pixel count (other dtypes are refused, never reinterpreted)."""
+    import numpy as np
+
+    if hasattr(a, "data_ptr"):
+        import torch
+
+        if a.is_cuda or not a.is_contiguous() or a.dtype != torch.float32:
+            raise FabfError(1, f"{name} must be a contiguous float32 host tensor")
+        n, p = a.numel(), a.data_ptr()
+    else:
+        if not isinstance(a, np.ndarray) or not a.flags["C_CONTIGUOUS"] or a.dtype != np.float32:
+            raise FabfError(1, f"{name} must be a contiguous float32 array")
+        n, p = a.size, a.ctypes.data
+    if n != _numel(plan.shape):
+        raise FabfError(1, f"{name} has {n} elements, the plan {plan.shape} needs {_numel(plan.shape)}")
+    return ctypes.c_void_p(p)
 
 
 def _stream_ptr(stream):
@@ -138,6 +167,12 @@ class Plan:
         _check(lib().fabf_last_fallback_count(self._h, ctypes.byref(c)))
         return int(c.value)
 
+    def last_launch_count(self) -> int:
+        """Kernels the last filter call on this plan launched."""
+        c = ctypes.c_int(0)
+        _check(lib().fabf_last_launch_count(self._h, ctypes.byref(c)))
+        return int(c.value)
+
     def debug_status(self):
         """FLAG_DEBUG plans: (violating pixels, first flat index or -1) of the last call."""
         c, f = ctypes.c_longlong(0), ctypes.c_longlong(0)
@@ -151,8 +186,8 @@ def filter(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=Non
 
     if out is None:
         out = torch.empty_like(img)
-    _check(lib().fabf_filter(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
-                             _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+    _check(lib().fabf_filter(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
+                             _dev_ptr(sigma, "sigma", plan), int(rho), int(N), _dev_ptr(out, "out", plan),
                              _stream_ptr(stream)))
     return out
 
@@ -166,8 +201,8 @@ def filter_diag(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, strea
     d = {k: torch.empty_like(img) for k in ("alpha", "beta", "kappa", "t2n")}
     d["code"] = torch.empty(img.shape, dtype=torch.uint8, device=img.device)
     diag = _Diag(*(ctypes.c_void_p(d[k].data_ptr()) for k in ("alpha", "beta", "kappa", "t2n", "code")))
-    _check(lib().fabf_filter_diag(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
-                                  _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+    _check(lib().fabf_filter_diag(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
+                                  _dev_ptr(sigma, "sigma", plan), int(rho), int(N), _dev_ptr(out, "out", plan),
                                   ctypes.byref(diag), _stream_ptr(stream)))
     return out, d
 
@@ -178,8 +213,8 @@ def bounds(plan: Plan, img, rho: int, alpha=None, beta=None, stream=None):
 
     alpha = torch.empty_like(img) if alpha is None else alpha
     beta = torch.empty_like(img) if beta is None else beta
-    _check(lib().fabf_bounds(plan.handle, _dev_ptr(img, "img"), int(rho), _dev_ptr(alpha, "alpha"),
-                             _dev_ptr(beta, "beta"), _stream_ptr(stream)))
+    _check(lib().fabf_bounds(plan.handle, _dev_ptr(img, "img", plan), int(rho), _dev_ptr(alpha, "alpha", plan),
+                             _dev_ptr(beta, "beta", plan), _stream_ptr(stream)))
     return alpha, beta
 
 
@@ -187,13 +222,7 @@ def filter_host(plan: Plan, img, theta, sigma, rho: int, N: int, out, stream=Non
     """fabf_filter_host on HOST buffers (numpy arrays or CPU tensors, ideally
     pinned); copies in, filters, copies out, synchronises."""
     def hp(a, name):
-        if hasattr(a, "data_ptr"):
-            if a.is_cuda or not a.is_contiguous():
-                raise FabfError(1, f"{name} must be a contiguous host tensor")
-            return ctypes.c_void_p(a.data_ptr())
-        if not a.flags["C_CONTIGUOUS"] or a.dtype.itemsize != 4:
-            raise FabfError(1, f"{name} must be contiguous float32")
-        return ctypes.c_void_p(a.ctypes.data)
+        return _host_ptr(a, name, plan)
 
     _check(lib().fabf_filter_host(plan.handle, hp(img, "img"), hp(theta, "theta"), hp(sigma, "sigma"),
                                   int(rho), int(N), hp(out, "out"), _stream_ptr(stream)))
@@ -210,8 +239,8 @@ def filter_events(plan: Plan, img, theta, sigma, rho: int, N: int, events, out=N
     if len(events) != 5:
         raise ValueError("five events")
     arr = (ctypes.c_void_p * 5)(*[ctypes.c_void_p(int(e.cuda_event)) for e in events])
-    _check(lib().fabf_filter_events(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
-                                    _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+    _check(lib().fabf_filter_events(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
+                                    _dev_ptr(sigma, "sigma", plan), int(rho), int(N), _dev_ptr(out, "out", plan),
                                     _stream_ptr(stream), arr))
     return out
 
@@ -223,7 +252,7 @@ def filter_profile(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, st
     if out is None:
         out = torch.empty_like(img)
     ms = (ctypes.c_float * 4)()
-    _check(lib().fabf_filter_profile(plan.handle, _dev_ptr(img, "img"), _dev_ptr(theta, "theta"),
-                                     _dev_ptr(sigma, "sigma"), int(rho), int(N), _dev_ptr(out, "out"),
+    _check(lib().fabf_filter_profile(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
+                                     _dev_ptr(sigma, "sigma", plan), int(rho), int(N), _dev_ptr(out, "out", plan),
                                      _stream_ptr(stream), ms))
     return out, [float(v) for v in ms]

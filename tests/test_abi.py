@@ -91,3 +91,21 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "fabf_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_binding_host_buffers_checked_without_gpu():
+    """The binding refuses host buffers that are not float32 or do not hold the
+    plan's pixel count (int32 would otherwise be reinterpreted as float)."""
+    import numpy as np
+
+    from paper_1811_02308_b200 import fabf
+
+    class _P:
+        shape = (1, 8, 8)
+
+    ok = np.zeros((1, 8, 8), np.float32)
+    assert fabf._host_ptr(ok, "img", _P()).value == ok.ctypes.data
+    for bad in (ok.astype(np.int32), ok.astype(np.float64), np.zeros((1, 8, 4), np.float32),
+                np.zeros((1, 8, 16), np.float32)[:, :, ::2]):
+        with pytest.raises(fabf.FabfError):
+            fabf._host_ptr(bad, "img", _P())

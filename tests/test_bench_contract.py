@@ -58,7 +58,9 @@ def test_gpu_arm_line():
     assert 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["e2e"]["value"] != d["value"]
-    assert d["gpu_launches"] == 3 * d["steps"]
+    assert d["gpu_launches"] == d["launches_per_step"] * d["steps"] and d["launches_per_step"] >= 1
+    assert r["alg_flops_per_pixel"] > 0 and abs(sum(r["regime_mix"].values()) - 1.0) < 1e-9
+    assert len(d["other_configs"]) == 3
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
     assert d["fallback_pixels"] == 0
