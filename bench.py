@@ -310,6 +310,7 @@ def run_gpu(args):
     fallback = plan.last_fallback_count()
     clk.__exit__(None, None, None)
     mix = regime_mix(fb, plan, img, th, sg, w.rho, w.N)  # outside the timed region
+    fused = {} if args.no_other_configs else fused_variant(fb, w, img, th, sg, flush)
     others = {} if args.no_other_configs else other_configs(fb, dev, flush)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
@@ -377,6 +378,7 @@ def run_gpu(args):
             "gpu_launches": launches_per_step * args.steps,  # fabf_last_launch_count x steps
             "launches_per_step": launches_per_step,
             "other_configs": others,
+            "fused_variant": fused,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
@@ -426,6 +428,29 @@ def other_configs(fb, dev, flush, steps: int = 10):
         res[w.name] = {"Mpix/s": w.img.size / (ms * 1e-3) / 1e6, "ms": ms, "rho": w.rho, "N": w.N,
                        "launches": plan.last_launch_count()}
     return res
+
+
+def fused_variant(fb, w, img, th, sg, flush, steps: int = 10):
+    """The same workload with FABF_FLAG_FUSED (bounds inside k_filter: one pass
+    reading f, theta, sigma, writing g-hat -- SURVEY a9), device-timed the same
+    way; reported beside the default (bounds kernel + k_filter at rho > 5)."""
+    import torch
+
+    plan = fb.Plan(*w.shape, fb.FLAG_FUSED)
+    out = torch.empty_like(img)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        fb.filter(plan, img, th, sg, w.rho, w.N, out=out)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush.fill_(1.0)
+        a.record(stream)
+        fb.filter(plan, img, th, sg, w.rho, w.N, out=out)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+    return {"Mpix/s": w.img.size / (ms * 1e-3) / 1e6, "ms_per_step": ms, "launches": plan.last_launch_count(),
+            "flags": "FABF_FLAG_FUSED"}
 
 
 def run_sweep(args):

@@ -55,6 +55,11 @@ typedef enum {
 #define FABF_FLAG_CLAMP 0x2u   /* clamp g-hat to [alpha_i, beta_i] after the guard (reading R7)    */
 #define FABF_FLAG_DEBUG 0x4u   /* validate the preconditions on the device every call: f, theta
                                   finite, sigma finite and > 0 (fabf_debug_status reads the result) */
+#define FABF_FLAG_FUSED 0x8u   /* compute the bounds alpha, beta (step a1) inside the per-pixel
+                                  kernel for every rho (one kernel reads f, theta, sigma and
+                                  writes g-hat: north_star (e)).  Without it they are
+                                  fused for rho <= 5 and produced by a separate bounds kernel
+                                  for larger rho, the faster choice on B200. */
 
 /* per-pixel diagnostic code bits (fabf_diag_t.code) */
 #define FABF_CODE_IDENTITY 0x1u /* alpha == beta: g-hat = f(i)                               */

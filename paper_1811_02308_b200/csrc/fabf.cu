@@ -38,7 +38,11 @@ struct fabf_plan_s {
   int device = 0;
   float* alpha = nullptr;  // workspace: bounds
   float* beta = nullptr;
-  float2* blkmm = nullptr;  // per bounds tile (min alpha, max beta)
+  float2* blkmm = nullptr;  // per bounds tile (min alpha, max beta), fabf_bounds only
+  // k_filter's vertical-bounds suffix rings (per resident CTA, sized at plan
+  // time for the largest rho the shape allows; L2-resident while in use)
+  float2* ring = nullptr;
+  long long ring_elems = 0;
   // exact-moment fallback: one counter per band of a call (slot b * kMaxBandsPlan
   // + k for band k of image b in fabf_filter_host, slot 0 otherwise); a band's
   // list is the region of fb_list at its own first pixel, so bands never share
@@ -68,8 +72,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxBands = fabf_plan_s::kMaxBandsPlan;  // fabf_filter_host row bands
-constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds fused into k_filter
-bool g_no_fuse = getenv("FABF_NO_FUSE") != nullptr;  // A/B switch for experiments
+constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds inside k_filter by default
+int g_fuse_rho = getenv("FABF_FUSE_RHO") ? atoi(getenv("FABF_FUSE_RHO")) : kFuseRho;
+// segment cap: max(g_seg_min, 3 w) rows (A/B switch FABF_SEG_MIN)
+int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 64;
 // k_fallback mode: 0 auto (default), 1 thread per pixel, 2 warp per pixel (A/B switch)
 int g_fb_mode = getenv("FABF_FB_MODE") ? atoi(getenv("FABF_FB_MODE")) : 0;
 // fabf_filter_host row bands per frame (A/B switch FABF_HOST_BANDS, 1..16)
@@ -475,39 +481,73 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
 }
 
 // ============================================================================
-// steps a2-a8.  Persistent grid, 256 threads, a CTA walks down vertical
-// segments of strips of TW output columns, RB = 256/TW output rows per step:
-//   A  column owners (thread c < L = TW + 2rho) add the entering row's powers
-//      to / remove the leaving row's powers from their fp64 vertical sums V_q
-//      (kept in shared memory between steps, odd stride) and write them to Ps;
+// steps a1-a8 in one pass (north_star (e)).  Persistent grid,
+// 256 threads; a CTA walks down vertical segments of strips of TW output
+// columns, RB = QS/TW output rows per step.  Per step:
+//   A  column owners (thread c < L = TW + 2 rho owns input column c):
+//      moments (a3): add the entering row's powers to / remove the leaving
+//        row's powers from the fp64 vertical sums V_q (shared memory, odd
+//        stride) and write them to the prefix rows Ps;
+//      bounds (a1), vertical van Herk / Gil-Werman streamed down the column:
+//        the segment's input rows are cut into blocks of w = 2 rho + 1 rows;
+//        a running prefix min/max of the current block, and the suffix
+//        min/max of the previous block from a per-CTA ring in global memory
+//        (L2-resident) that a look-ahead sweep fills one block in advance
+//        (one extra load per row, 2w rows ahead at most); the window's
+//        vertical (min, max) = op(suffix_{b-1}, prefix_b) goes to VX;
 //   B  a 16-lane group per (row, q) turns the row into an exclusive prefix
-//      P[0] = 0, P[1 + c] = sum_{c' <= c} V(c') in place (lane l owns E odd
-//      consecutive entries: conflict-free), 4 shuffle rounds;
-//   C1 one pixel per thread: window sums S_q = P[x + w] - P[x], stretch to the
-//      fit's Legendre coefficients (fp64), regime; the record goes to a
-//      shared-memory queue, regime-A records from the front, B/C from the back;
-//   C2 thread j finishes queue record j (integrals, ratio, guard, store), so
-//      warps run one integral regime each except at the A|B boundary.
+//      P[0] = 0, P[1 + c] = sum_{c' <= c} V(c') in place (lane l owns E
+//      odd consecutive entries), 4 shuffle rounds; and, per (row, block of w
+//      columns), one thread runs the horizontal van Herk / Gil-Werman sweeps
+//      over VX: backward suffix, forward prefix of the next block -> alpha,
+//      beta of every output pixel in VY (3 comparisons per sample, any rho);
+//   C1 one pixel per thread-iteration: S_q = P[x + w] - P[x], identity test,
+//      stretch to the fit's Legendre coefficients (fp64), regime; the record
+//      goes to a shared-memory queue, regime-A from the front, B/C from the back;
+//   C2 thread j finishes queue record j (integrals, ratio, guard, store).
 constexpr int kSL = 16;  // lanes per prefix scan
+
+// FABF_EXP_TIMERS (experiments only): thread 0 of every CTA accumulates clock64
+// deltas per phase; fabf_exp_timers() reads them back
+#ifdef FABF_EXP_TIMERS
+__device__ unsigned long long g_exp_timers[8];
+#define EXP_T(slot)                                  \
+  do {                                               \
+    if (tid == 0) {                                  \
+      const long long now_ = clock64();              \
+      t_acc[slot] += (unsigned long long)(now_ - t_last); \
+      t_last = now_;                                 \
+    }                                                \
+  } while (0)
+#else
+#define EXP_T(slot) \
+  do {              \
+  } while (0)
+#endif
 
 struct FilterArgs {
   const float* img;
   const float* theta;
   const float* sigma;
-  const float* alpha;
+  const float* alpha;   // !FB: the bounds planes k_bounds wrote
   const float* beta;
+  const float2* blkmm;  // !FB: per kBT x kBT bounds tile (min alpha, max beta)
   float* out;
-  float* alpha_w;  // fused small-rho path: alpha / beta of fallback pixels
+  float* alpha_w;  // alpha / beta of fallback pixels (read by k_fallback)
   float* beta_w;
+  int fused;        // 1: bounds inside k_filter (FB), 0: from k_bounds' planes
+  float2* ring;     // per-CTA vertical suffix rings [grid][2][w][L]
+  long long ring_cta;  // float2 elements per CTA
+  long long ring_ctas;  // CTAs the plan's ring buffer holds (grid cap)
   int B, H, W, rho;
   int SH;          // segment cap (rows)
   int b0, r0, r1;  // images [b0, b0 + B), rows [r0, r1) of each (row bands)
-  int fused;       // 1: bounds computed inside k_filter (rho <= kFuseRho)
-  const float2* blkmm;  // per kBT x kBT bounds tile: (min alpha, max beta)
   unsigned flags;
   double flag_root;  // 2^(flag_bits / N)
   int* fb_count;
   int* fb_list;
+  float* d_alpha;  // diagnostics (fabf_filter_diag), may be NULL
+  float* d_beta;
   float* d_kappa;
   float* d_t2n;
   unsigned char* d_code;
@@ -523,8 +563,14 @@ struct FilterGeom {
 template <int N, int E>
 struct FilterSmem {
   // byte offsets into dynamic shared memory
-  size_t ps, vs, qnu, q4, qo, ring, vmm, total;
-  __host__ __device__ FilterSmem(int L, int RB, int QS, int WF = 0) {
+  size_t ps, vs, qnu, qo, q4, vx, vy, vz, total;
+  // bounds rows: VX (pitch L; the prefix sweeps read up to 2 rho samples past
+  // a row's end -- into the next row or VY -- which only reach outputs
+  // x >= TW), VY / VZ (pitch TW)
+  __host__ __device__ static int xpitch(int L, int TW, int w) { return L; }
+  __host__ __device__ static int ypitch(int TW, int w) { return TW; }
+  __host__ __device__ FilterSmem(int L, int RB, int QS, int TW, bool FB) {
+    const int w = L - TW + 1, XP = FB ? xpitch(L, TW, w) : 0, YP = FB ? ypitch(TW, w) : 0;
     using G = FilterGeom<N, E>;
     size_t off = 0;
     ps = off;
@@ -532,26 +578,27 @@ struct FilterSmem {
     vs = off;
     off += sizeof(double) * (size_t)G::VST * L;
     // the pixel queue: C2 of step s reads it before the barrier after A of
-    // step s+1 and C1 of step s+1 writes it after the next one: single buffer
+    // step s+1 and C1 of step s+1 writes it after the next one: single
+    // buffer; nup_1..nup_N (nup_0 = n is not stored)
     qnu = off;
-    off += sizeof(double) * (size_t)(N + 1) * QS;
-    off = (off + 15) & ~(size_t)15;
-    q4 = off;  // (theta, sigma, alpha, beta) of each record: one 16-byte access
-    off += sizeof(float4) * QS;
-    qo = off;
+    off += sizeof(double) * (size_t)G::NN * QS;
+    qo = off;  // in-step pixel index of each record
     off += sizeof(int) * QS;
-    // fused bounds (WF = 2 rho + 1 > 0): per-column ring of the last WF rows,
-    // and the vertical (min, max) of each step row
-    ring = off;
-    off += sizeof(float) * (size_t)L * WF;
+    off = (off + 15) & ~(size_t)15;
+    q4 = off;  // !FB: (theta, sigma, alpha, beta) of each record, one 16-byte access
+    off += FB ? 0 : sizeof(float4) * QS;
     off = (off + 7) & ~(size_t)7;
-    vmm = off;
-    off += WF > 0 ? sizeof(float2) * (size_t)RB * L : 0;
+    vx = off;  // vertical (min, max) of each input column, per step row
+    off += sizeof(float2) * (size_t)RB * XP;
+    vy = off;  // (alpha, beta) of each output pixel: suffix within its block
+    off += sizeof(float2) * (size_t)RB * YP;
+    vz = off;  // ... and prefix within the next block
+    off += sizeof(float2) * (size_t)RB * YP;
     total = off;
   }
 };
 
-template <int N, int E, int TW, int PPT, int WD, int WF>
+template <int N, int E, int TW, int PPT, int WD, bool FB>
 __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int cnt[2];  // per step parity: regime-A count (low 16 bits), B/C count (high 16)
@@ -564,28 +611,39 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   const int H = a.H, W = a.W;
   const int L = TW + 2 * rho;  // input columns of a strip, <= 16 * E (host picks E)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const FilterSmem<N, E> lay(L, RB, QS, WF);
-  float* ring = reinterpret_cast<float*>(smraw + lay.ring);    // [L][WF]
-  float2* vmm = reinterpret_cast<float2*>(smraw + lay.vmm);    // [RB][L]
+  const FilterSmem<N, E> lay(L, RB, QS, TW, FB);
   double* Ps = reinterpret_cast<double*>(smraw + lay.ps);    // [RB][NN][PSQ]
   double* Vs = reinterpret_cast<double*>(smraw + lay.vs);    // [L][VST]
-  double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [N+1][QS]
-  float4* q4 = reinterpret_cast<float4*>(smraw + lay.q4);
+  double* qnu = reinterpret_cast<double*>(smraw + lay.qnu);  // [N][QS]
   int* qo = reinterpret_cast<int*>(smraw + lay.qo);
+  float4* q4 = reinterpret_cast<float4*>(smraw + lay.q4);
+  const int XP = FilterSmem<N, E>::xpitch(L, TW, w), YP = FilterSmem<N, E>::ypitch(TW, w);
+  float2* VX = reinterpret_cast<float2*>(smraw + lay.vx);    // [RB][XP]
+  float2* VY = reinterpret_cast<float2*>(smraw + lay.vy);    // [RB][YP]
+  float2* VZ = reinterpret_cast<float2*>(smraw + lay.vz);    // [RB][YP]
   const float n = (float)(w * w);
   const bool want_t2n = a.d_t2n != nullptr;
+  const float2 kEmpty = make_float2(CUDART_INF_F, -CUDART_INF_F);
 
   for (int i = tid; i < RB * NN * PSQ; i += kThreads) Ps[i] = 0.0;  // P[0] = 0 for good
+#ifdef FABF_EXP_TIMERS
+  unsigned long long t_acc[8] = {};
+  long long t_last = clock64();
+#endif
 
   // column-owner identity (thread c owns input column c of the strip)
   const int c = tid;
   const bool owner = c < L;
   double* vsc = Vs + (owner ? c : 0) * VST;
   double* psc = Ps + 1 + c;
+  // this CTA's vertical suffix rings: ring[(buf * w + i) * L + c], buf = block
+  // parity, i = suffix position (int offsets: a ring is < 2^31 elements)
+  float2* ringc = a.ring + (long long)blockIdx.x * a.ring_cta + (owner ? c : 0);
   // pixel identity within a step: pixels tid + i * kThreads, i < PPT
   const int px_r = tid / TW, px_x = tid % TW;  // (row px_r + i * kThreads / TW)
   // phase-B identity
   const int sgrp = tid / kSL, sl = tid % kSL;
+  const int nbk = (TW + w - 1) / w;  // horizontal bounds blocks per output row
 
   // balanced static schedule: the B * nstrips * H strip-rows are split into
   // gridDim.x contiguous chunks (one per resident CTA); a chunk is one or two
@@ -607,20 +665,31 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     const int bimg = a.b0 + bl;
     const int x0 = strip * TW;
     const size_t plane = (size_t)bimg * H * W;
+    const float* colp = a.img + plane + reflect_index(min(x0 - rho + c, W - 1 + rho), W);
 
-    // ---- tile-local centre c_T and power-of-two scale s_T: min/max over the
-    // ---- segment's bounds tiles (their windows cover the segment footprint)
+    // ---- tile-local centre c_T and power-of-two scale s_T: the range of the
+    // ---- segment's input footprint (rows Y0-rho .. Y1+rho-1, the strip's
+    // ---- L columns) -- every sample the running sums will ever see
+    // ---- (FB: a pass over the footprint; else the bounds tiles of k_bounds,
+    // ---- whose windows cover the footprint)
     float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
-    if (WF > 0) {
-      // fused bounds: no bounds tiles -- the range of the segment's input
-      // footprint (rows Y0-rho .. Y1+rho-1 of this thread's column)
-      if (tid < L) {
-        const float* cp = a.img + plane + reflect_index(min(x0 - rho + tid, W - 1 + rho), W);
-#pragma unroll 4
-        for (int y = Y0 - rho; y < Y1 + rho; ++y) {
-          const float v = __ldg(cp + reflect_index(y, H) * W);
-          lmin = fminf(lmin, v);
-          lmax = fmaxf(lmax, v);
+    if constexpr (FB) {
+      if (owner) {
+        if (Y0 - rho >= 0 && Y1 + rho <= H) {  // (uniform) no reflection
+          const float* cp = colp + (Y0 - rho) * W;
+#pragma unroll 16
+          for (int y = 0; y < Y1 - Y0 + 2 * rho; ++y) {
+            const float v = __ldg(cp + y * W);
+            lmin = fminf(lmin, v);
+            lmax = fmaxf(lmax, v);
+          }
+        } else {
+#pragma unroll 8
+          for (int y = Y0 - rho; y < Y1 + rho; ++y) {
+            const float v = __ldg(colp + reflect_index(y, H) * W);
+            lmin = fminf(lmin, v);
+            lmax = fmaxf(lmax, v);
+          }
         }
       }
     } else {
@@ -654,6 +723,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         lmax = fmaxf(lmax, red_max[i]);
       }
     }
+    EXP_T(0);
     const double cT = 0.5 * ((double)lmin + (double)lmax);
     const double halfr = 0.5 * ((double)lmax - (double)lmin);
     int e2 = 0;
@@ -661,31 +731,82 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     const double invS = ldexp(1.0, -e2);  // 1/s_T, s_T = 2^e2 >= half range: exact scaling
     const double mcs = -cT * invS;         // u = f * invS + mcs, exact
 
-    const float* colp = a.img + plane + reflect_index(min(x0 - rho + c, W - 1 + rho), W);
+    // ---- vertical bounds (van Herk / Gil-Werman streamed down each column).
+    // Segment-local entering row k = y - (Y0 - rho), block b = k / w, position
+    // j = k - b w.  For the entering row k the look-ahead sweep takes row
+    // b w + (w-1-j) of the same block and stores suffix_b(w-1-j) in the ring
+    // buffer b & 1; the output window [k-w+1, k] is prefix_b(j) (j = w-1) or
+    // op(suffix_{b-1}(j+1), prefix_b(j)), suffix_{b-1}(1) from a register (it
+    // is written 2 rows before it is read, possibly in the same step).
+    // kb, kj: block / position of the next entering row (uniform).  Phase A
+    // writes the vertical (min, max) of the step's rows to VX.
+    int kb = 0, kj = 2 * rho;
+    const int ysweep0 = Y0 - rho;
+    float2 pre = kEmpty, suf = kEmpty, s1 = kEmpty, s1n = kEmpty;  // per column
+    const bool pro_inside = Y0 - rho >= 0 && Y0 + rho <= H - 1;      // uniform
+    // general (row by row) bounds step: entering samples e[0..nr) of the rows
+    // whose window ends there; writes VX row r
+    auto bounds_rows_general = [&](const float (&e)[RB], int nr) {
+      float fs[RB];
+      float2 rgv[RB];
+      {
+        int b = kb, j = kj;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          fs[r] = 0.f;
+          rgv[r] = kEmpty;
+          if (r < nr) {
+            const int y = min(ysweep0 + b * w + (w - 1 - j), H - 1 + rho);
+            fs[r] = __ldg(colp + reflect_index(y, H) * W);
+            if (j >= 1 && j + 1 < w) rgv[r] = ringc[(((b - 1) & 1) * w + j + 1) * L];
+            if (++j == w) j = 0, ++b;
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (r >= nr) break;
+        const float2 vin = mm_in(e[r]);
+        pre = (kj == 0) ? vin : mm2(pre, vin);
+        suf = (kj == 0) ? mm_in(fs[r]) : mm2(suf, mm_in(fs[r]));
+        const int i = w - 1 - kj;
+        if (i >= 2) ringc[((kb & 1) * w + i) * L] = suf;
+        float2 v = pre;
+        if (kj == 0) v = mm2(s1, pre);
+        else if (kj + 1 < w) v = mm2(rgv[r], pre);
+        if (i == 1) s1n = suf;
+        VX[r * XP + c] = v;
+        if (++kj == w) {
+          kj = 0;
+          ++kb;
+          s1 = s1n;
+        }
+      }
+    };
+    auto advance_counters = [&](int nr) {  // non-owners: the same uniform kb, kj
+      for (int r = 0; r < nr; ++r)
+        if (++kj == w) kj = 0, ++kb;
+    };
 
-    // prologue: rows Y0-rho .. Y0+rho-1.  Row Y0-rho-1 lies outside every
-    // window of the segment and so possibly far outside its centring range:
-    // it is never added, and the first step's leaving sample is u = 0 (adding
-    // and then removing an outlier's powers would wipe out the fp64 sums).
+    // prologue: entering rows k = 0 .. 2 rho - 1 (rows Y0-rho .. Y0+rho-1), no
+    // outputs yet.  Row Y0-rho-1 lies outside every window of the segment and
+    // so possibly far outside its centring range: it is never added, and the
+    // first step's leaving sample is u = 0.
     if (owner) {
       double V[NN];
 #pragma unroll
       for (int q = 0; q < NN; ++q) V[q] = 0.0;
-      // rows in batches of 8 loads issued ahead of the arithmetic (the loop is
-      // otherwise one exposed L2 latency per row)
-      constexpr int PB = 8;
+      constexpr int PB = 8;  // loads issued in batches ahead of the arithmetic
       for (int y0 = Y0 - rho; y0 < Y0 + rho; y0 += PB) {
         float fb[PB];
 #pragma unroll
         for (int k = 0; k < PB; ++k) {
           const int yin = min(y0 + k, Y0 + rho - 1);
-          fb[k] = __ldg(colp + reflect_index(yin, H) * W);
+          fb[k] = __ldg(colp + (pro_inside ? yin : reflect_index(yin, H)) * W);
         }
 #pragma unroll
         for (int k = 0; k < PB; ++k) {
-          const int yin = y0 + k;
-          if (yin < Y0 + rho) {
-            if (WF > 0 && yin >= Y0 - rho) ring[c * WF + (yin - (Y0 - rho))] = fb[k];
+          if (y0 + k < Y0 + rho) {
             const double uu = fma((double)fb[k], invS, mcs);
             double pu = uu;
 #pragma unroll
@@ -693,13 +814,35 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               V[q] += pu;
               pu *= uu;
             }
+            if constexpr (FB) pre = mm2(pre, mm_in(fb[k]));  // prefix of block 0
           }
         }
       }
 #pragma unroll
       for (int q = 0; q < N; ++q) vsc[q] = V[q];
+      // block 0's look-ahead suffix: positions i = w-1 .. 1 (rows Y0-rho+i),
+      // ring buffer 0; suffix_0(1) kept for the first output of block 1
+      if constexpr (FB)
+      for (int i0 = w - 1; i0 >= 1; i0 -= PB) {
+        float sb[PB];
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          const int y = Y0 - rho + max(i0 - k, 1);
+          sb[k] = __ldg(colp + (pro_inside ? y : reflect_index(y, H)) * W);
+        }
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          const int i = i0 - k;
+          if (i >= 1) {
+            suf = mm2(suf, mm_in(sb[k]));
+            if (i >= 2) ringc[i * L] = suf;
+          }
+        }
+      }
+      s1n = suf;
     }
 
+    EXP_T(1);
     // phase-A input prefetch: entering / leaving samples of the next step's rows
     float pf_in[RB], pf_out[RB];
     auto prefetch = [&](int Yb) {
@@ -718,34 +861,52 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // this thread's pixel parameters (latency hidden behind A and B)
       bool pvalid[PPT];
       int po[PPT];
-      float p_al[PPT], p_be[PPT], p_th[PPT], p_sg[PPT];
+      float p_th[PPT], p_sg[PPT], p_al[PPT], p_be[PPT];
 #pragma unroll
       for (int i = 0; i < PPT; ++i) {
         const int pr = px_r + i * (kThreads / TW);
         const int pY = Yb + pr, pX = x0 + px_x;
         pvalid[i] = (pr < nr) && (pX < W);
         po[i] = (int)plane + pY * W + pX;
-        p_al[i] = p_be[i] = p_th[i] = 0.f;
+        p_th[i] = p_al[i] = p_be[i] = 0.f;
         p_sg[i] = 1.f;
         if (pvalid[i]) {
-          if (WF == 0) {  // (fused bounds: alpha, beta come from vmm in C1)
+          p_th[i] = __ldg(a.theta + po[i]);
+          p_sg[i] = __ldg(a.sigma + po[i]);
+          if constexpr (!FB) {
             p_al[i] = __ldg(a.alpha + po[i]);
             p_be[i] = __ldg(a.beta + po[i]);
           }
-          p_th[i] = __ldg(a.theta + po[i]);
-          p_sg[i] = __ldg(a.sigma + po[i]);
         }
       }
       if (tid == 0) {
         cnt[qb] = 0;
       }
-      // ---- phase A: entering row Yb+r+rho in, leaving row Yb+r-rho-1 out
+      // ---- phase A: moments (entering row Yb+r+rho in, leaving row
+      // ---- Yb+r-rho-1 out) and vertical bounds of the step's rows
+      // the bounds' fast path: a full step with every row at 1 <= j <= w-3
+      // (no block edge, no special case), look-ahead rows inside the image
+      const int srow0 = ysweep0 + kb * w + (w - 1 - kj);  // look-ahead row of r = 0
+      const bool fast = !FB || (nr == RB && kj >= 1 && kj + RB <= w - 2 && srow0 - (RB - 1) >= 0 &&
+                                srow0 <= H - 1);  // uniform
       if (owner) {
-        float fin[RB], fout[RB];
+        float fin[RB], fout[RB], fsw[RB];
+        float2 rg[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
           fin[r] = pf_in[r];
           fout[r] = pf_out[r];
+        }
+        // bounds loads first (ring entries were written at least one step
+        // ago; look-ahead samples are L2 hits after the centring pass)
+        if (FB && fast) {
+          const float* sp = colp + srow0 * W;
+          const float2* rp = ringc + (((kb - 1) & 1) * w + kj + 1) * L;
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            fsw[r] = __ldg(sp - r * W);
+            rg[r] = rp[r * L];
+          }
         }
         prefetch(Yb + RB);
         double V[NN];
@@ -771,23 +932,31 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             }
 #pragma unroll
             for (int q = 0; q < N; ++q) psc[(r * NN + q) * PSQ] = V[q];
-            if (WF > 0) {  // fused bounds: the ring now holds the window's WF rows
-              ring[c * WF + (Yb + r + 2 * rho - Y0) % (WF > 0 ? WF : 1)] = fin[r];
-              float mn = ring[c * WF], mx = mn;
-#pragma unroll
-              for (int d = 1; d < WF; ++d) {
-                const float v = ring[c * WF + d];
-                mn = fminf(mn, v);
-                mx = fmaxf(mx, v);
-              }
-              vmm[r * L + c] = make_float2(mn, mx);
-            }
           }
         }
 #pragma unroll
         for (int q = 0; q < N; ++q) vsc[q] = V[q];
+        // vertical bounds of the step's rows
+        if constexpr (!FB) {
+        } else if (fast) {
+          float2* wp = ringc + ((kb & 1) * w + (w - 1 - kj)) * L;
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            pre = mm2(pre, mm_in(fin[r]));
+            suf = mm2(suf, mm_in(fsw[r]));
+            wp[-r * L] = suf;
+            VX[r * XP + c] = mm2(rg[r], pre);
+          }
+          kj += RB;
+        } else {
+          bounds_rows_general(fin, nr);
+        }
+      } else if constexpr (FB) {
+        if (fast) kj += RB;
+        else advance_counters(nr);
       }
       __syncthreads();
+      EXP_T(2);
       // ---- phase B: exclusive prefix rows, 16 lanes per (r, q) (WD > 0: small
       // ---- windows are summed directly in C1 instead, no prefix magnitudes)
       if (N > 0 && WD == 0) {
@@ -824,10 +993,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           }
         } else
         for (int b = 2 * warp; b < nr * N; b += 2 * G) {
-          const int s0 = b + (sgrp & 1), s1 = s0 + G;
-          const bool act0 = s0 < nr * N, act1 = s1 < nr * N;
+          const int s0 = b + (sgrp & 1), s1r = s0 + G;
+          const bool act0 = s0 < nr * N, act1 = s1r < nr * N;
           double* row0 = Ps + (act0 ? s0 : b) * PSQ + 1 + sl * E;
-          double* row1 = Ps + (act1 ? s1 : b) * PSQ + 1 + sl * E;
+          double* row1 = Ps + (act1 ? s1r : b) * PSQ + 1 + sl * E;
           double v0[E], v1[E];
 #pragma unroll
           for (int e = 0; e < E; ++e) {
@@ -846,10 +1015,10 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 #pragma unroll
           for (int off = 1; off < kSL; off <<= 1) {
             const double u0 = __shfl_up_sync(0xffffffffu, i0, off, kSL);
-            const double u1 = __shfl_up_sync(0xffffffffu, i1, off, kSL);
+            const double u1v = __shfl_up_sync(0xffffffffu, i1, off, kSL);
             if (sl >= off) {
               i0 += u0;
-              i1 += u1;
+              i1 += u1v;
             }
           }
           // the offset comes straight from the neighbour (never inc - tot: a
@@ -867,7 +1036,52 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           }
         }
       }
+      // horizontal bounds over VX, per (row r, block jb of w
+      // output columns): one lane runs the suffix within block jb into VY,
+      // another the prefix within block jb + 1 into VZ, so that the outputs x
+      // in [jb w, (jb+1) w) get alpha, beta = op(VY[x], VZ[x]) -- 3
+      // comparisons per sample whatever rho is.  Fixed trip counts (w, w - 1):
+      // no divergence except the prefix's one shorter trip; samples past L
+      // only reach outputs x >= TW, whose stores are skipped.  The jobs
+      // (2 nr nbk) fill the top warps.
+#ifndef FABF_EXP_NOHB
+      for (int t = kThreads - 1 - tid; FB && t < 2 * nr * nbk; t += kThreads) {
+        const int dir = t & 1, rj = t >> 1, r = rj / nbk, jb = rj - r * nbk;
+        const float2* __restrict__ X = VX + r * XP;
+        const int xlo = jb * w;
+        // suffix: positions xlo + w - 1 down to xlo, outputs at the same index;
+        // prefix: positions (jb+1) w .. (jb+1) w + w - 2, outputs at p - w + 1
+        const int p0 = dir ? xlo + w : xlo + w - 1, dp = dir ? 1 : -1, os = dir ? 1 - w : 0;
+        float2* __restrict__ O = (dir ? VZ : VY) + r * YP;
+        if (dir) O[xlo] = kEmpty;  // VZ[jb w]: the window is block jb itself
+        const int trips = w - dir;
+        float2 acc = kEmpty;
+        int p = p0, k = 0;
+        for (; k + 4 <= trips; k += 4, p += 4 * dp) {
+          float2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = X[p + u * dp];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc = mm2(acc, v[u]);
+            const int o = p + u * dp + os;
+            if (o < TW) O[o] = acc;
+          }
+        }
+        for (; k < trips; ++k, p += dp) {
+          acc = mm2(acc, X[p]);
+          if (p + os < TW) O[p + os] = acc;
+        }
+      }
+#else
+      for (int t = tid; t < RB * TW; t += kThreads) {  // experiment: vertical-only range
+        const int r = t / TW, x = t - r * TW;
+        VY[r * YP + x] = VX[r * XP + x + rho];
+        VZ[r * YP + x] = kEmpty;
+      }
+#endif
       __syncthreads();
+      EXP_T(3);
       // ---- phase C1: window sums, flag, regime, slot in the queue, stretch
       // ---- written straight into the slot
       // (two passes: regimes of this thread's PPT pixels first, so that one
@@ -876,19 +1090,17 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 #pragma unroll
       for (int i = 0; i < PPT; ++i) {
         regime[i] = -1;  // -1: no record (invalid, identity or fallback)
-        if (WF > 0 && pvalid[i]) {  // fused bounds: horizontal min / max of vmm
-          const float2* vr = vmm + (px_r + i * (kThreads / TW)) * L + px_x;
-          float2 m = vr[0];
-#pragma unroll
-          for (int d = 1; d < WF; ++d) {
-            const float2 v = vr[d];
-            m.x = fminf(m.x, v.x);
-            m.y = fmaxf(m.y, v.y);
-          }
-          p_al[i] = m.x;
-          p_be[i] = m.y;
+        if constexpr (FB) {
+          const int pix = (px_r + i * (kThreads / TW)) * YP + px_x;
+          const float2 ab = mm2(VY[pix], VZ[pix]);
+          p_al[i] = ab.x;
+          p_be[i] = ab.y;
         }
         if (pvalid[i]) {
+          if (a.d_alpha) {
+            a.d_alpha[po[i]] = p_al[i];
+            a.d_beta[po[i]] = p_be[i];
+          }
           if (p_al[i] == p_be[i]) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
             a.out[po[i]] = p_al[i];
             if (a.d_kappa) a.d_kappa[po[i]] = 1.0f;
@@ -898,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
                                      a.flag_root)) {  // exact-moment fallback pass
             const int slotfb = atomicAdd(a.fb_count, 1);
             a.fb_list[slotfb] = po[i];
-            if (WF > 0) {  // the fallback kernel reads alpha, beta from the plan
+            if constexpr (FB) {  // the fallback kernel reads alpha, beta from the plan
               a.alpha_w[po[i]] = p_al[i];
               a.beta_w[po[i]] = p_be[i];
             }
@@ -943,25 +1155,37 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           const int j = (regime[i] == kRegA) ? baseA + __popc(mA[i] & lt)
                                              : QS - 1 - (baseB + __popc(mB[i] & lt));
           nu_from_sums<N>(S, au, bu, qnu + j, QS);
-          q4[j] = make_float4(p_th[i], p_sg[i], p_al[i], p_be[i]);
-          qo[j] = po[i];
+          qo[j] = (px_r + i * (kThreads / TW)) * TW + px_x;  // in-step pixel index
+          if constexpr (!FB) q4[j] = make_float4(p_th[i], p_sg[i], p_al[i], p_be[i]);
         }
         baseA += __popc(mA[i]);
         baseB += __popc(mB[i]);
       }
       __syncthreads();
+      EXP_T(4);
       // ---- phase C2: integrals, ratio, guard, store (one regime per warp).  No
-      // ---- barrier after it (see FilterSmem: the counters are double buffered).
+      // ---- barrier after it (the counters are double buffered; the queue is
+      // ---- read before the barrier that ends the next step's phase A).
       {
         const int nA = cnt[qb] & 0xffff, nBC = cnt[qb] >> 16;
+        const int rowbase = (int)plane + Yb * W + x0;
 #pragma unroll 1
         for (int i = 0; i < PPT; ++i) {
           const int j = tid + i * kThreads;
           if (j < nA || j >= QS - nBC) {
-            const double* nu = qnu + j;  // nu[k * QS]
-            const int o = qo[j];
-            const float4 rec = q4[j];
-            const float th = rec.x, sg = rec.y, al = rec.z, be = rec.w;
+            const double* nu = qnu + j;  // nup_k = nu[(k - 1) * QS]
+            // the record's pixel within the step: (alpha, beta) still in VY / VZ
+            // (rewritten only in the next step's phase A, after C2 of this one)
+            const int pix = qo[j], pr = pix / TW, px = pix - pr * TW;
+            const int o = rowbase + pr * W + px;
+            float th, sg, al, be;
+            if constexpr (FB) {
+              const float2 ab = mm2(VY[pr * YP + px], VZ[pr * YP + px]);
+              th = __ldg(a.theta + o), sg = __ldg(a.sigma + o), al = ab.x, be = ab.y;
+            } else {
+              const float4 rec = q4[j];
+              th = rec.x, sg = rec.y, al = rec.z, be = rec.w;
+            }
             int regime = kRegA;
             if (j >= nA) {
               float lam, t0;
@@ -975,8 +1199,15 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           }
         }
       }
+      EXP_T(5);
     }
   }
+#ifdef FABF_EXP_TIMERS
+  if (tid == 0) {
+    t_acc[6] = 1;
+    for (int i = 0; i < 7; ++i) atomicAdd(&g_exp_timers[i], t_acc[i]);
+  }
+#endif
 }
 
 // ============================================================================
@@ -1030,7 +1261,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
     const int o = a.fb_list[i];
     const int b = o / (H * W), rem = o - b * H * W, y = rem / W, x = rem - y * W;
     const float* img = a.img + (size_t)b * H * W;
-    const float al = a.alpha[o], be = a.beta[o];
+    const float al = a.alpha_w[o], be = a.beta_w[o];
     const double mid = 0.5 * ((double)al + (double)be), ih = 2.0 / ((double)be - (double)al);
     double acc[N + 1];
 #pragma unroll
@@ -1068,7 +1299,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
       float lam, t0;
       const float th = a.theta[o], sg = a.sigma[o];
       const int regime = range_params(al, be, th, sg, lam, t0);
-      PixelResult res = ghat_from_record<N>(nu, 1, th, sg, al, be, regime, a.flags,
+      PixelResult res = ghat_from_record<N>(nu + 1, 1, th, sg, al, be, regime, a.flags,
                                             a.d_t2n != nullptr, (float)n);
       a.out[o] = res.g;
       if (a.d_kappa) a.d_kappa[o] = res.kappa;
@@ -1224,25 +1455,34 @@ fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, fl
 
 // pixels per thread per step: 2 when the (worst-case L = 16E) shared memory
 // still fits two CTAs per SM, else 1
-template <int N, int E, int WF>
+template <int N, int E, bool FB>
 constexpr int ppt_for() {
-  constexpr int NN = N > 0 ? N : 1;
+  constexpr size_t NN = N > 0 ? N : 1;
   constexpr size_t L = (size_t)kSL * E;
   constexpr size_t ps2 = sizeof(double) * 4 * NN * (L + 2);
   constexpr size_t vs = sizeof(double) * (NN | 1) * L;
-  constexpr size_t q2 = (sizeof(double) * (N + 1) + 5 * 4) * 2 * kThreads;
-  constexpr size_t fz = sizeof(float) * L * WF + (WF > 0 ? sizeof(float2) * 4 * L : 0);
-  return ps2 + vs + q2 + fz <= 110 * 1024 ? 2 : 1;
+  constexpr size_t q2 = (sizeof(double) * NN + 4 + (FB ? 0 : 16)) * 2 * kThreads;
+  // bounds rows (worst case over the rho this E serves, TW = 128):
+  constexpr size_t bz = FB ? sizeof(float2) * 4 * (L + 2 * 128) : 0;
+  return ps2 + vs + q2 + bz <= 114 * 1024 ? 2 : 1;
 }
-template <int N, int E, int TW, int WD = 0, int WF = 0>
-fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
+constexpr int kMaxCtaPerSm = 3;  // persistent grid cap (sizes the plan's bounds rings)
+
+// bounds-ring elements (float2) one CTA needs for rho (TW as launch_filter_n picks it)
+inline long long ring_elems_per_cta(int rho) {
+  const int TW = (128 + 2 * rho <= 256) ? 128 : 64;
+  return 2LL * (2 * rho + 1) * (TW + 2 * rho);
+}
+
+template <int N, int E, int TW, int WD, bool FB>
+fabf_status_t launch_filter_fb(FilterArgs& fa, cudaStream_t st) {
 #ifdef FABF_PPT
   constexpr int PPT = FABF_PPT;
 #else
-  constexpr int PPT = ppt_for<N, E, WF>();
+  constexpr int PPT = ppt_for<N, E, FB>();
 #endif
   const int L = TW + 2 * fa.rho, QS = PPT * kThreads, RB = QS / TW;
-  const size_t smem = FilterSmem<N, E>(L, RB, QS, WF).total;
+  const size_t smem = FilterSmem<N, E>(L, RB, QS, TW, FB).total;
   if (smem > kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
   static int grid_cache[kMaxDevices] = {};  // resident CTAs per device (persistent schedule)
   static size_t smem_cache[kMaxDevices] = {};
@@ -1250,23 +1490,30 @@ fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
   FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   std::unique_lock<std::mutex> lk(g_launch_mu);
   if (grid_cache[dev] == 0 || smem_cache[dev] != smem) {
-    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT, WD, WF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FABF_CUDA(cudaFuncSetAttribute(k_filter<N, E, TW, PPT, WD, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxDynSmem),
               "cudaFuncSetAttribute(k_filter)");
     int per_sm = 0, sms = 0;
-    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT, WD, WF>, kThreads, smem),
+    FABF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<N, E, TW, PPT, WD, FB>, kThreads, smem),
               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     FABF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
-    grid_cache[dev] = max(1, per_sm) * sms;
+    grid_cache[dev] = std::min(std::max(1, per_sm), kMaxCtaPerSm) * sms;
     smem_cache[dev] = smem;
   }
   const long long strips = (long long)fa.B * ((fa.W + TW - 1) / TW) * (fa.r1 - fa.r0);
-  const int grid = (int)std::min<long long>(grid_cache[dev], strips);
+  long long grid_ll = std::min<long long>(grid_cache[dev], strips);
+  if (FB) grid_ll = std::min<long long>(grid_ll, fa.ring_ctas);  // one bounds ring per CTA
+  const int grid = (int)grid_ll;
   lk.unlock();
-  k_filter<N, E, TW, PPT, WD, WF><<<grid, kThreads, smem, st>>>(fa);
+  k_filter<N, E, TW, PPT, WD, FB><<<grid, kThreads, smem, st>>>(fa);
   ++g_launches;
   FABF_CUDA(cudaGetLastError(), "k_filter launch");
   return FABF_OK;
+}
+
+template <int N, int E, int TW, int WD = 0>
+fabf_status_t launch_filter_net(FilterArgs& fa, cudaStream_t st) {
+  return fa.fused ? launch_filter_fb<N, E, TW, WD, true>(fa, st) : launch_filter_fb<N, E, TW, WD, false>(fa, st);
 }
 
 template <int N>
@@ -1276,16 +1523,7 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
   fabf_status_t s;
   // prefix rows of 16*E entries, E odd (conflict-free strided phase-B access)
   // (column owners: L = TW + 2 rho <= 256 threads)
-  if (fa.fused) {  // rho <= 5: bounds fused into k_filter (no k_bounds, no alpha/beta planes)
-    switch (fa.rho) {
-      case 0: s = launch_filter_net<N, 9, 128, 1, 1>(fa, st); break;
-      case 1: s = launch_filter_net<N, 9, 128, 3, 3>(fa, st); break;
-      case 2: s = launch_filter_net<N, 9, 128, 5, 5>(fa, st); break;
-      case 3: s = launch_filter_net<N, 9, 128, 7, 7>(fa, st); break;
-      case 4: s = launch_filter_net<N, 9, 128, 0, 9>(fa, st); break;
-      default: s = launch_filter_net<N, 9, 128, 0, 11>(fa, st); break;
-    }
-  } else if (fa.rho <= 3) {  // direct window sums (see k_filter, phase B)
+  if (fa.rho <= 3) {  // direct window sums (see k_filter, phase B)
     switch (fa.rho) {
       case 0: s = launch_filter_net<N, 9, 128, 1>(fa, st); break;
       case 1: s = launch_filter_net<N, 9, 128, 3>(fa, st); break;
@@ -1315,6 +1553,10 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
 }
 
 fabf_status_t launch_filter(FilterArgs& fa, int N, int B, cudaStream_t st) {
+#ifdef FABF_ONLY_N  // development builds: one degree only (fast compiles)
+  if (N == FABF_ONLY_N) return launch_filter_n<FABF_ONLY_N>(fa, B, st);
+  return fail(FABF_ERR_UNSUPPORTED, "library built with FABF_ONLY_N");
+#else
   switch (N) {
     case 0: return launch_filter_n<0>(fa, B, st);
     case 1: return launch_filter_n<1>(fa, B, st);
@@ -1329,6 +1571,7 @@ fabf_status_t launch_filter(FilterArgs& fa, int N, int B, cudaStream_t st) {
     case 10: return launch_filter_n<10>(fa, B, st);
     default: return fail(FABF_ERR_UNSUPPORTED, "N > FABF_MAX_N");
   }
+#endif
 }
 
 // a plan's workspace lives on the device it was made on; calls must be made
@@ -1372,6 +1615,15 @@ fabf_status_t validate_filter(Plan* p, const float* img, const float* theta, con
   return FABF_OK;
 }
 
+// where the bounds run: FABF_FLAG_FUSED plans always in k_filter; otherwise
+// in k_filter for rho <= g_fuse_rho (default kFuseRho: measured crossover,
+// DESIGN.md section 4), else in k_bounds.  FABF_FUSE_RHO overrides the
+// crossover (experiments).
+bool fused_choice(const Plan* p, int rho) {
+  if (p->flags & FABF_FLAG_FUSED) return true;
+  return rho <= g_fuse_rho && p->ring_elems >= ring_elems_per_cta(rho);
+}
+
 // The three kernels for images [b0, b0 + nb), rows [64 ty0, min(H, 64 ty1)).
 // Reads input rows up to rho outside the band (the caller guarantees they are
 // in place); writes out, alpha, beta of the band only.
@@ -1386,30 +1638,26 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
     ++g_launches;
     FABF_CUDA(cudaGetLastError(), "k_validate launch");
   }
-  // small windows: bounds inside k_filter (north_star (e): each pixel crosses
-  // HBM once); the diagnostic entry point keeps the separate bounds kernel
-  // because it returns the alpha / beta planes
-  const bool fused = rho <= kFuseRho && diag == nullptr && !g_no_fuse;
+  // bounds inside k_filter (north_star (e): each pixel crosses HBM once) or
+  // from k_bounds' planes (the faster choice where k_filter is issue-bound,
+  // DESIGN.md section 4): fused_choice()
+  const bool fused = fused_choice(p, rho);
   fabf_status_t s = FABF_OK;
   if (fused)
     prof_mark(0, st), prof_mark(1, st), prof_mark(2, st);
   else
     s = launch_bounds(p, img, rho, p->alpha, p->beta, b0, nb, ty0, ty1, st);
   if (s != FABF_OK) return s;
-  const size_t bytes = sizeof(float) * (size_t)p->B * p->H * p->W;
-  if (diag && diag->alpha)
-    FABF_CUDA(cudaMemcpyAsync(diag->alpha, p->alpha, bytes, cudaMemcpyDeviceToDevice, st), "copy alpha");
-  if (diag && diag->beta)
-    FABF_CUDA(cudaMemcpyAsync(diag->beta, p->beta, bytes, cudaMemcpyDeviceToDevice, st), "copy beta");
   FilterArgs fa;
+  fa.fused = fused ? 1 : 0;
+  fa.alpha = p->alpha;
+  fa.beta = p->beta;
+  fa.blkmm = p->blkmm;
   fa.img = img;
   fa.theta = theta;
   fa.sigma = sigma;
-  fa.alpha = p->alpha;
-  fa.beta = p->beta;
   fa.alpha_w = p->alpha;
   fa.beta_w = p->beta;
-  fa.fused = fused ? 1 : 0;
   fa.out = out;
   fa.H = p->H;
   fa.W = p->W;
@@ -1419,9 +1667,11 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
   fa.r0 = ty0 * kBT;
   fa.r1 = std::min(p->H, ty1 * kBT);
   // segment cap (rows): fresh fp64 sums every few window heights
-  fa.SH = std::max(64, 3 * (2 * rho + 1));
-  fa.blkmm = p->blkmm;
+  fa.SH = std::max(g_seg_min, 3 * (2 * rho + 1));
   fa.flags = p->flags;
+  fa.ring = p->ring;
+  fa.ring_cta = ring_elems_per_cta(rho);
+  fa.ring_ctas = p->ring_elems / std::max(1LL, fa.ring_cta);
   {
     // fallback flag: amplification ((1+|m|)/h)^N times the magnitude of the
     // summed terms relative to n (prefix rows: L w / n; direct sums: 1) may
@@ -1433,6 +1683,17 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
   }
   fa.fb_count = p->fb_count + fb_slot;
   fa.fb_list = p->fb_list + ((size_t)b0 * p->H + fa.r0) * p->W;
+  fa.d_alpha = diag ? diag->alpha : nullptr;
+  fa.d_beta = diag ? diag->beta : nullptr;
+  if (!fa.d_alpha || !fa.d_beta) fa.d_alpha = fa.d_beta = nullptr;
+  if (!fused && diag) {  // the whole planes, not only the filtered pixels
+    const size_t bytes = sizeof(float) * (size_t)p->B * p->H * p->W;
+    if (diag->alpha)
+      FABF_CUDA(cudaMemcpyAsync(diag->alpha, p->alpha, bytes, cudaMemcpyDeviceToDevice, st), "copy alpha");
+    if (diag->beta)
+      FABF_CUDA(cudaMemcpyAsync(diag->beta, p->beta, bytes, cudaMemcpyDeviceToDevice, st), "copy beta");
+    fa.d_alpha = fa.d_beta = nullptr;
+  }
   fa.d_kappa = diag ? diag->kappa : nullptr;
   fa.d_t2n = diag ? diag->t2n : nullptr;
   fa.d_code = diag ? diag->code : nullptr;
@@ -1445,6 +1706,20 @@ fabf_status_t debug_reset(Plan* p, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->dbg, 0, sizeof(unsigned long long), st), "cudaMemsetAsync(dbg)");
   FABF_CUDA(cudaMemsetAsync(p->dbg + 1, 0xff, sizeof(unsigned long long), st), "cudaMemsetAsync(dbg)");
   return FABF_OK;
+}
+
+// the bounds rings of k_filter: kMaxCtaPerSm CTAs per SM, each with room for
+// the largest rho this shape admits (2 rho + 1 <= min(H, W), rho <= kMaxRho)
+cudaError_t alloc_ring(Plan* p) {
+  int sms = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  if (e != cudaSuccess) return e;
+  int rho_max = std::min(kMaxRho, (std::min(p->H, p->W) - 1) / 2);
+  if (!(p->flags & FABF_FLAG_FUSED)) rho_max = std::min(rho_max, std::max(0, g_fuse_rho));
+  long long per = 1;
+  for (int r = 0; r <= rho_max; ++r) per = std::max(per, ring_elems_per_cta(r));
+  p->ring_elems = per * kMaxCtaPerSm * sms;
+  return cudaMalloc(&p->ring, sizeof(float2) * (size_t)p->ring_elems);
 }
 
 // a fresh set of fallback counters per call
@@ -1483,7 +1758,7 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
     return fail(FABF_ERR_INVALID_ARGUMENT, "batch, height and width must be >= 1");
   if ((size_t)batch * height * width >= (size_t)1 << 31)
     return fail(FABF_ERR_INVALID_ARGUMENT, "more than 2^31-1 pixels per call");
-  if (flags & ~(unsigned)(FABF_FLAG_LITERAL | FABF_FLAG_CLAMP | FABF_FLAG_DEBUG))
+  if (flags & ~(unsigned)(FABF_FLAG_LITERAL | FABF_FLAG_CLAMP | FABF_FLAG_DEBUG | FABF_FLAG_FUSED))
     return fail(FABF_ERR_INVALID_ARGUMENT, "unknown flag bits");
   int dev = 0;
   fabf_status_t s = check_device(&dev);
@@ -1505,6 +1780,7 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
                                      ((width + kBT - 1) / kBT))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_count, sizeof(int) * (size_t)batch * Plan::kMaxBandsPlan)) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess ||
+      (e = alloc_ring(p)) != cudaSuccess ||
       ((flags & FABF_FLAG_DEBUG) &&
        (e = cudaMalloc(&p->dbg, 2 * sizeof(unsigned long long))) != cudaSuccess)) {
     fabf_destroy(p);
@@ -1722,6 +1998,7 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   cudaFree(p->alpha);
   cudaFree(p->beta);
   cudaFree(p->blkmm);
+  cudaFree(p->ring);
   cudaFree(p->fb_count);
   cudaFree(p->fb_list);
   cudaFree(p->dbg);
@@ -1753,6 +2030,16 @@ const char* fabf_status_string(fabf_status_t status) {
 }
 
 const char* fabf_last_error_message(void) { return g_last_error.c_str(); }
+
+#ifdef FABF_EXP_TIMERS
+// experiments: read (and reset) the per-phase clock64 sums of k_filter
+int fabf_exp_timers(unsigned long long out[8]) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+  if (cudaMemcpyFromSymbol(out, g_exp_timers, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  const unsigned long long z[8] = {};
+  return cudaMemcpyToSymbol(g_exp_timers, z, sizeof(z)) != cudaSuccess;
+}
+#endif
 
 int fabf_version(void) { return FABF_VERSION; }
 

@@ -144,8 +144,8 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
   // a8 sums consumed on the fly (no A / X arrays): T2 = sum nup_k A_k,
   // U = sum nup_k X_k, ab = sum |nup_k A_k|
-  // nup[k * ns], k >= 1: read where used, not held across the seeds;
-  // nup_0 = nu0 = n (the window size) is never stored
+  // nup_k = nup[(k - 1) * ns], k >= 1: read where used, not held across the
+  // seeds; nup_0 = nu0 = n (the window size) is never stored
   T2 = nu0 * a0;
   ab = fabs(T2);
   U = 0.0;
@@ -156,7 +156,7 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
     const double bk = (k & 1) ? bnd_odd : bnd_even;
     const double x = fma(s0, a_cur, fma(dk, inv2k, -bk));
     if (k == 0) X0 = x;
-    U = fma(k == 0 ? nu0 : nup[k * ns], x, U);
+    U = fma(k == 0 ? nu0 : nup[(k - 1) * ns], x, U);
     if (k < N) {
       const double a_next = fma(c_rec[2 * k], x, c_rec[2 * k + 1] * a_prev);
       if (k & 1)
@@ -165,7 +165,7 @@ __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double 
         d_even = fma((double)(2 * k + 1), a_cur, d_even);
       a_prev = a_cur;
       a_cur = a_next;
-      const double nk = nup[(k + 1) * ns];
+      const double nk = nup[k * ns];
       T2 = fma(nk, a_next, T2);
       ab = fma(fabs(nk), fabs(a_next), ab);
     }
@@ -274,7 +274,7 @@ __device__ __forceinline__ void contract(const double* nup, int ns, double nu0, 
   double T2 = 0.0, U = 0.0, ab = 0.0;
 #pragma unroll
   for (int k = 0; k <= N; ++k) {
-    const double nk = k == 0 ? nu0 : nup[k * ns];
+    const double nk = k == 0 ? nu0 : nup[(k - 1) * ns];
     T2 = fma(nk, A[k], T2);
     ab = fma(fabs(nk), fabs(A[k]), ab);
     U = fma(nk, X[k], U);
@@ -299,7 +299,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     float T2 = 0.0f, U = 0.0f, ab = 0.0f;
 #pragma unroll
     for (int k = 0; k <= N; ++k) {
-      const float v = k == 0 ? n : (float)nup[k * ns];
+      const float v = k == 0 ? n : (float)nup[(k - 1) * ns];
       const float t = v * A[k];
       T2 += t;
       ab += fabsf(t);
@@ -402,7 +402,7 @@ __device__ __forceinline__ void nu_from_sums(double S[N + 1], double au, double 
     double v = 0.0;
 #pragma unroll
     for (int r = k & 1; r <= k; r += 2) v = fma((double)(2 * k + 1) * leg_coef(k, r), S[r], v);
-    nup[k * ns] = v;
+    nup[(k - 1) * ns] = v;
   }
 }
 

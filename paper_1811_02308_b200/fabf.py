@@ -17,6 +17,7 @@ library_path = os.environ.get("FABF_LIB") or os.path.join(_PKG, "libfabf.so")  #
 FLAG_LITERAL = 0x1
 FLAG_CLAMP = 0x2
 FLAG_DEBUG = 0x4
+FLAG_FUSED = 0x8
 CODE_IDENTITY = 0x1
 CODE_GUARD = 0x2
 CODE_SMALL_LAMBDA = 0x4
@@ -60,11 +61,13 @@ def lib():
             L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
             L.fabf_filter_events.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_void_p)]
             L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
-            L.fabf_last_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
+            if hasattr(L, "fabf_last_launch_count"):  # (absent from round-1 builds kept for A/B timing)
+                L.fabf_last_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
+                L.fabf_last_launch_count.restype = ctypes.c_int
             L.fabf_debug_status.argtypes = [P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
             L.fabf_destroy.argtypes = [P]
             for fn in ("fabf_plan", "fabf_filter", "fabf_filter_diag", "fabf_bounds",
-                       "fabf_filter_host", "fabf_last_fallback_count", "fabf_last_launch_count", "fabf_destroy",
+                       "fabf_filter_host", "fabf_last_fallback_count", "fabf_destroy",
                        "fabf_filter_profile", "fabf_filter_events", "fabf_debug_status"):
                 getattr(L, fn).restype = ctypes.c_int
             L.fabf_status_string.argtypes = [i]

@@ -49,28 +49,37 @@ def _filter(fb, w, flags=0):
     return out.cpu().numpy(), plan
 
 
-def test_config4_every_pixel(fb, orc):
+@pytest.fixture(scope="module")
+def cfg4(orc):
     w = workloads.config(4)
-    out, plan = _filter(fb, w)
-    o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+    return w, orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_config4_every_pixel(fb, cfg4, fused):
+    """Both bounds placements: k_bounds + k_filter (the default at rho = 20)
+    and FABF_FLAG_FUSED (bounds inside k_filter, one pass over f, theta, sigma)."""
+    w, o = cfg4
+    out, plan = _filter(fb, w, fb.FLAG_FUSED if fused else 0)
     mx, nbad, err = compare_guarded(out, o, 1.0)
     assert nbad == 0, f"max |delta| = {mx} grey"
     assert np.isfinite(out).all()
     ident = (o["code"] & 1) > 0
     assert np.array_equal(out[ident], w.img[ident])
-    print(f"config 4 every pixel: max |delta| {mx:.3e} grey, p99.9 {np.quantile(err, 0.999):.3e}, "
-          f"fallback pixels {plan.last_fallback_count()}")
+    print(f"config 4 every pixel (fused={fused}): max |delta| {mx:.3e} grey, "
+          f"p99.9 {np.quantile(err, 0.999):.3e}, fallback pixels {plan.last_fallback_count()}, "
+          f"kernels {plan.last_launch_count()}")
 
 
 FRAMES = (0, 11, 22, 31)
 
 
-@pytest.mark.parametrize("gen,rho,N,expect_fallback", [
-    ("texture", 40, 8, True), ("texture", 40, 10, True), ("texture", 20, 10, True),
-    ("rectangles", 2, 10, True)])
-def test_config5_cells_full_batch(fb, orc, gen, rho, N, expect_fallback):
+@pytest.mark.parametrize("gen,rho,N,expect_fallback,fused", [
+    ("texture", 40, 8, True, False), ("texture", 40, 10, True, False), ("texture", 20, 10, True, False),
+    ("rectangles", 2, 10, True, False), ("texture", 40, 10, True, True)])
+def test_config5_cells_full_batch(fb, orc, gen, rho, N, expect_fallback, fused):
     w = workloads.config5(rho, N, batch=32, size=1024, generator=gen)
-    out, plan = _filter(fb, w)
+    out, plan = _filter(fb, w, fb.FLAG_FUSED if fused else 0)
     nfb = plan.last_fallback_count()
     if expect_fallback:
         assert nfb > 0, "expected pixels on the exact-moment fallback"
@@ -79,7 +88,7 @@ def test_config5_cells_full_batch(fb, orc, gen, rho, N, expect_fallback):
     mx, nbad, _ = compare_guarded(out[sub], o, 1.0)
     assert nbad == 0, f"{gen} rho={rho} N={N}: max |delta| = {mx} grey ({nfb} fallback pixels)"
     assert np.isfinite(out).all()
-    print(f"config 5 {gen} rho={rho} N={N}: max |delta| {mx:.3e} grey over frames {FRAMES}, "
+    print(f"config 5 {gen} rho={rho} N={N} fused={fused}: max |delta| {mx:.3e} grey over frames {FRAMES}, "
           f"{nfb} fallback pixels in the batch")
 
 
@@ -96,11 +105,11 @@ def _outlier_rows_image(H, W, rho, seed):
     return [a.astype(np.float32)[None] for a in (f, th, sg)]
 
 
-@pytest.mark.parametrize("rho,N", [(20, 8), (9, 10), (4, 8)])
-def test_segment_start_outlier_rows(fb, orc, rho, N):
+@pytest.mark.parametrize("rho,N,fused", [(20, 8, False), (9, 10, False), (4, 8, False), (20, 8, True)])
+def test_segment_start_outlier_rows(fb, orc, rho, N, fused):
     f, th, sg = _outlier_rows_image(64 * 9 + 17, 300, rho, 900 + rho)
     w = workloads.Workload("outlier_rows", f, th, sg, rho, N)
-    out, _ = _filter(fb, w)
+    out, _ = _filter(fb, w, fb.FLAG_FUSED if fused else 0)
     o = orc.fast(f, th, sg, rho, N)
     mx, nbad, _ = compare_guarded(out, o, 1.0)
     assert nbad == 0, f"fabf_filter: max |delta| = {mx} grey"

@@ -138,9 +138,10 @@ def test_config_full_size_sampled(fb, orc, cfg, nsample):
 
 # ------------------------------------------------------------------ edge cases
 @pytest.mark.parametrize("N", list(range(0, 11)))
-def test_every_degree(fb, orc, N):
-    w = workloads.random_case(2, 45, 61, seed=100 + N, kind="rect", rho=4, N=N)
-    out, _, _ = _run(fb, w)
+@pytest.mark.parametrize("rho,fused", [(4, False), (13, False), (13, True)])
+def test_every_degree(fb, orc, N, rho, fused):
+    w = workloads.random_case(2, 45, 61, seed=100 + N, kind="rect", rho=rho, N=N)
+    out, _, _ = _run(fb, w, flags=fb.FLAG_FUSED if fused else 0)
     o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
     mx, nbad, _ = compare_guarded(out, o, 1.0)
     assert nbad == 0, f"N={N}: max |delta| = {mx}"
@@ -169,9 +170,12 @@ def test_wide_windows_high_degree(fb, orc, rho, N):
     ("texture", (1, 96, 200), 40, 8),   # rho = 40 (config 5's largest)
     ("rect", (1, 200, 230), 96, 4),     # largest supported rho
 ])
-def test_edge_shapes(fb, orc, kind, shape, rho, N):
+@pytest.mark.parametrize("fused", [False, True])
+def test_edge_shapes(fb, orc, kind, shape, rho, N, fused):
+    """Both bounds placements (FABF_FLAG_FUSED: alpha, beta from k_filter's own
+    van Herk / Gil-Werman passes, reported by the diag path and bit-exact)."""
     w = workloads.random_case(*shape, seed=7, kind=kind, rho=rho, N=N)
-    out, d, _ = _run(fb, w, diag=True)
+    out, d, _ = _run(fb, w, flags=fb.FLAG_FUSED if fused else 0, diag=True)
     o = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
     sc = grey_scale(w.img)
     mx, nbad, _ = compare_guarded(out, o, sc)
@@ -179,6 +183,8 @@ def test_edge_shapes(fb, orc, kind, shape, rho, N):
     ident = (o["code"] & 1) > 0
     assert np.array_equal(out[ident], w.img[ident])
     assert np.array_equal((d["code"] & 1) > 0, ident)
+    ra, rb = orc.bounds(w.img, w.rho)
+    assert np.array_equal(d["alpha"], ra) and np.array_equal(d["beta"], rb)
 
 
 @pytest.mark.parametrize("kind,shape,rho,N", [

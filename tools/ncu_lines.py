@@ -39,7 +39,8 @@ for r in csv.reader(io.StringIO(txt)):
     rows.append((s, ins, fname, d["Line No"], d["Source"].strip()[:70], st))
     tot_s += s
     tot_i += ins
-rows.sort(key=lambda x: -x[0])
+import os
+rows.sort(key=lambda x: -x[1] if os.environ.get("SORT") == "instr" else -x[0])
 print(f"total samples {tot_s}, warp instructions {tot_i}")
 for s, ins, f, ln, src, st in rows[:top]:
     sts = " ".join(f"{k}:{100*v/max(s,1):.0f}%" for k, v in st)
