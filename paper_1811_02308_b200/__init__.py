@@ -21,6 +21,7 @@ from .fabf import (  # noqa: F401
     FLAG_LITERAL,
     FLAG_CLAMP,
     FLAG_DEBUG,
+    FLAG_FUSED,
     CODE_IDENTITY,
     CODE_GUARD,
     CODE_SMALL_LAMBDA,

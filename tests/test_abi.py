@@ -109,3 +109,15 @@ def test_binding_host_buffers_checked_without_gpu():
                 np.zeros((1, 8, 16), np.float32)[:, :, ::2]):
         with pytest.raises(fabf.FabfError):
             fabf._host_ptr(bad, "img", _P())
+
+
+def test_binding_constants_match_header():
+    """Every FABF_FLAG_* / FABF_CODE_* of include/fabf.h is exported by the
+    package with the same value (the binding hard-codes them)."""
+    import paper_1811_02308_b200 as fb
+
+    src = open(HEADER).read()
+    found = re.findall(r"#define\s+FABF_((?:FLAG|CODE)_[A-Z_]+)\s+(0x[0-9a-fA-F]+)u?", src)
+    assert found
+    for name, val in found:
+        assert getattr(fb, name) == int(val, 16), name
