@@ -311,6 +311,7 @@ def run_gpu(args):
     clk.__exit__(None, None, None)
     mix = regime_mix(fb, plan, img, th, sg, w.rho, w.N)  # outside the timed region
     fused = {} if args.no_other_configs else fused_variant(fb, w, img, th, sg, flush)
+    colour = {} if args.no_other_configs else colour_variant(fb, dev, flush)
     others = {} if args.no_other_configs else other_configs(fb, dev, flush)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
@@ -379,6 +380,7 @@ def run_gpu(args):
             "launches_per_step": launches_per_step,
             "other_configs": others,
             "fused_variant": fused,
+            "colour_variant": colour,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
@@ -451,6 +453,40 @@ def fused_variant(fb, w, img, th, sg, flush, steps: int = 10):
     ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
     return {"Mpix/s": w.img.size / (ms * 1e-3) / 1e6, "ms_per_step": ms, "launches": plan.last_launch_count(),
             "flags": "FABF_FLAG_FUSED"}
+
+
+def colour_variant(fb, dev, flush, steps: int = 10):
+    """NEXT-3: a 3840x2160 RGB frame (channel-interleaved fp32; the channels are
+    the config-4 image, a shifted copy and its negative), rho = 20, N = 8, through
+    fabf_filter_interleaved (channel by channel); device-timed,
+    colour pixels (3 channels) per second."""
+    import torch
+
+    import workloads
+
+    rng = np.random.default_rng(4242)
+    base = workloads.config(4).img[0]
+    img = np.stack([base, np.roll(base, 97, axis=1), 255 - base], axis=-1)
+    th = (img + rng.uniform(-15, 15, img.shape)).astype(np.float32)
+    sg = rng.uniform(5, 60, img.shape).astype(np.float32)
+    H, W, C = img.shape
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev)
+    img_d, th_d, sg_d = t(img), t(th), t(sg)
+    out = torch.empty_like(img_d)
+    plan = fb.Plan(C, H, W)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        fb.filter_interleaved(plan, img_d, th_d, sg_d, 20, 8, out=out)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush.fill_(1.0)
+        a.record(stream)
+        fb.filter_interleaved(plan, img_d, th_d, sg_d, 20, 8, out=out)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+    return {"workload": "3840x2160x3 interleaved RGB, rho=20, N=8", "colour Mpix/s": H * W / (ms * 1e-3) / 1e6,
+            "plane Mpix/s": C * H * W / (ms * 1e-3) / 1e6, "ms_per_frame": ms, "launches": plan.last_launch_count()}
 
 
 def run_sweep(args):

@@ -128,6 +128,29 @@ fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* al
 fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
                                const float* sigma, int rho, int N, float* out, void* stream);
 
+/* The baseline the paper compares with (NEXT-4): Mozerov & van de Weijer's
+ * uniform-prior filter with Delta = 0 (Fig.3) -- eq.(29) at
+ * N = 0 fitted on [f(i), 2 fbar(i) - f(i)] (fbar = the box mean over the same
+ * (2 rho + 1)^2 window) instead of [alpha_i, beta_i]; f(i) where that interval
+ * is a point.  Same arguments, pointer rules and errors as fabf_filter
+ * (without N); FABF_FLAG_LITERAL / CLAMP do not apply (the N = 0 ratio needs
+ * no guard).                                                                  */
+fabf_status_t fabf_filter_mozerov(fabf_plan_t plan, const float* img, const float* theta,
+                                  const float* sigma, int rho, float* out, void* stream);
+
+/* Colour / multi-channel images, filtered channel by channel as the paper does
+ * (P:855): img, theta, sigma and out are DEVICE buffers of B/C images of
+ * height x width x `channels` fp32, channel-interleaved (pixel-major, the
+ * usual RGB layout), 16-byte alignment not required.  The plan's batch B
+ * counts planes (images x channels) and must be a multiple of `channels`.
+ * The channels are moved to plan-owned planar buffers (allocated on first
+ * use, shared with fabf_filter_host), filtered as a batch of planes exactly
+ * as fabf_filter would, and moved back.  Asynchronous on `stream`.  Errors as
+ * fabf_filter, plus INVALID_ARGUMENT if `channels` does not divide the batch. */
+fabf_status_t fabf_filter_interleaved(fabf_plan_t plan, const float* img, const float* theta,
+                                      const float* sigma, int channels, int rho, int N, float* out,
+                                      void* stream);
+
 /* Number of pixels the last fabf_filter* call on this plan routed to the
  * exact-moment fallback (synchronises the plan's stream to read it).         */
 fabf_status_t fabf_last_fallback_count(fabf_plan_t plan, long long* count);

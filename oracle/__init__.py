@@ -15,6 +15,8 @@ from .oracle import (  # noqa: F401
     fit,
     hilbert_inverse,
     integrals,
+    literal,
+    mozerov,
     stretch,
     CODE_IDENTITY,
     CODE_GUARD,

@@ -511,3 +511,143 @@ int fabfo_fast(const float* img, const float* theta, const float* sigma, int B, 
   free(vals);
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* O3 "literal": Algorithm 1 as printed, in plain fp64, with the   */
+/* paper's own scaling (f, theta, sigma divided by 255 before, g-hat times 255 */
+/* after).  CONTEXT ONLY -- it is not a parity target: it shows how */
+/* far the paper's own numerics drift from the __float128 reference above.     */
+/*   line 2  alpha, beta: window min / max (eq.(8); exhaustive scan -- the same  */
+/*           values the O(1) MAX-FILTER gives);                                 */
+/*   line 6  gamma_k = omega * f^k, k = 0..N, omega = 1/n on the box (gamma_0 =  */
+/*           1), by O(1) separable running sums in fp64 (the paper's      */
+/*           recursive-filter route);                                    */
+/*   line 9  mu from m = gamma by eq.(24);                            */
+/*   line 11 c = A^{-1} mu with eq.(19) in fp64;                         */
+/*   lines 12-14 t0, lambda, I_0 by eq.(31) (C99 erf), I_1 by eq.(32);          */
+/*   lines 17-20 I_k by the forward recursion eq.(30) for every lambda;          */
+/*   line 21 g-hat = alpha + (beta - alpha) T1/T2 (no guard, eq.(29)).           */
+/* Identity (alpha == beta) pixels copy f (lines 4-5).  Whole images only (the  */
+/* running sums need every row).                                               */
+int fabfo_literal(const float* img, const float* theta, const float* sigma, int B, int H, int W,
+                  int rho, int N, double* g) {
+  if (!img || !theta || !sigma || !g || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
+  if (2 * rho + 1 > H || 2 * rho + 1 > W || N < 0 || N > FABFO_MAX_N) return 1;
+  const long HW = (long)H * W;
+  const int w = 2 * rho + 1;
+  const double inv_n = 1.0 / ((double)w * w);
+  double* rowsum = (double*)malloc(sizeof(double) * (size_t)HW * (N + 1));
+  double* gam = (double*)malloc(sizeof(double) * (size_t)HW * (N + 1));
+  float* amin = (float*)malloc(sizeof(float) * (size_t)HW);
+  float* bmax = (float*)malloc(sizeof(float) * (size_t)HW);
+  if (!rowsum || !gam || !amin || !bmax) {
+    free(rowsum), free(gam), free(amin), free(bmax);
+    return 2;
+  }
+  double Ainv[(FABFO_MAX_N + 1) * (FABFO_MAX_N + 1)];
+  fabfo_hilbert_inverse(N, Ainv);
+  for (long b = 0; b < B; ++b) {
+    const float* f = img + b * HW;
+    fabfo_bounds(f, 1, H, W, rho, 0, HW, amin, bmax);
+    /* horizontal running sums of (f/255)^k (reflected borders, reading R2) */
+    for (long y = 0; y < H; ++y)
+      for (int k = 0; k <= N; ++k) {
+        double s = 0;
+        for (long dx = -rho; dx <= rho; ++dx) s += pow((double)f[y * W + reflect_index(dx, W)] / 255.0, k);
+        rowsum[((size_t)k * H + y) * W + 0] = s;
+        for (long x = 1; x < W; ++x) {
+          s += pow((double)f[y * W + reflect_index(x + rho, W)] / 255.0, k) -
+               pow((double)f[y * W + reflect_index(x - rho - 1, W)] / 255.0, k);
+          rowsum[((size_t)k * H + y) * W + x] = s;
+        }
+      }
+    /* vertical running sums, times omega = 1/n */
+    for (int k = 0; k <= N; ++k)
+      for (long x = 0; x < W; ++x) {
+        const double* R = rowsum + (size_t)k * HW;
+        double s = 0;
+        for (long dy = -rho; dy <= rho; ++dy) s += R[reflect_index(dy, H) * W + x];
+        gam[(size_t)k * HW + x] = s * inv_n;
+        for (long y = 1; y < H; ++y) {
+          s += R[reflect_index(y + rho, H) * W + x] - R[reflect_index(y - rho - 1, H) * W + x];
+          gam[(size_t)k * HW + y * W + x] = s * inv_n;
+        }
+      }
+    for (long p = 0; p < HW; ++p) {
+      const double al = amin[p] / 255.0, be = bmax[p] / 255.0;
+      if (amin[p] == bmax[p]) { /* lines 4-5 */
+        g[b * HW + p] = f[p];
+        continue;
+      }
+      const double d = be - al;
+      double mu[FABFO_MAX_N + 1], c[FABFO_MAX_N + 1];
+      for (int k = 0; k <= N; ++k) { /* eq.(24) */
+        double s = 0;
+        for (int r = 0; r <= k; ++r) s += (double)binom_q(k, r) * pow(-al, k - r) * gam[(size_t)r * HW + p];
+        mu[k] = s / pow(d, k);
+      }
+      for (int m = 0; m <= N; ++m) { /* c = A^{-1} mu */
+        double s = 0;
+        for (int n2 = 0; n2 <= N; ++n2) s += Ainv[m * (N + 1) + n2] * mu[n2];
+        c[m] = s;
+      }
+      const double t0 = (theta[b * HW + p] / 255.0 - al) / d;
+      const double sg = sigma[b * HW + p] / 255.0;
+      const double lam = 0.5 * d * d / (sg * sg);
+      const double sl = sqrt(lam);
+      const double E1 = exp(-lam * (1 - t0) * (1 - t0));
+      double I0 = 0.5 * sqrt(M_PI / lam) * (erf(sl * (1 - t0)) - erf(-sl * t0)); /* eq.(31) */
+      double I1 = t0 * I0 + (exp(-lam * t0 * t0) - E1) / (2 * lam);            /* eq.(32) */
+      double T1 = c[0] * I1, T2 = c[0] * I0;
+      double Ikm2 = I0, Ikm1 = I1;
+      for (int k = 2; k <= N + 1; ++k) { /* eq.(30) */
+        const double Ik = t0 * Ikm1 + (k - 1) / (2 * lam) * Ikm2 - E1 / (2 * lam);
+        T1 += c[k - 1] * Ik;
+        T2 += c[k - 1] * Ikm1;
+        Ikm2 = Ikm1;
+        Ikm1 = Ik;
+      }
+      g[b * HW + p] = 255.0 * (al + d * (T1 / T2));
+    }
+  }
+  free(rowsum), free(gam), free(amin), free(bmax);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Mozerov & van de Weijer's uniform-prior filter as the paper compares it    */
+/* (Fig.3): a constant (degree-0) fit of the local histogram */
+/* on [f(i), 2 fbar(i) - f(i)] (Delta = 0, the narrowest valid uniform         */
+/* distribution; fbar = the Omega-mean, omega = 1 on the box, reading R1)      */
+/* instead of [alpha_i, beta_i]:  with [a, b] that interval in increasing      */
+/* order, t0 = (theta - a)/(b - a), lambda = (b - a)^2 / (2 sigma^2),          */
+/*   g_moz = a + (b - a) I_1 / I_0                          (eq.(29) at N = 0) */
+/* and g_moz = f(i) when a = b.  __float128 throughout (the window mean is a   */
+/* direct sum); integrals as for fabfo_fast.                                   */
+int fabfo_mozerov(const float* img, const float* theta, const float* sigma, int B, int H, int W,
+                  int rho, long p0, long p1, double* g) {
+  if (!img || !theta || !sigma || !g || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
+  if (2 * rho + 1 > H || 2 * rho + 1 > W) return 1;
+  const long HW = (long)H * W;
+  const int n = (2 * rho + 1) * (2 * rho + 1);
+  float* vals = (float*)malloc(sizeof(float) * (size_t)n);
+  if (!vals) return 2;
+  for (long p = p0; p < p1; ++p) {
+    const long b = p / HW, r = p % HW, y = r / W, x = r % W;
+    gather_window(img, H, W, rho, b, y, x, vals);
+    qd s = 0;
+    for (int j = 0; j < n; ++j) s += vals[j];
+    const qd fb = s / n, f = img[p], e = 2 * fb - f;
+    const qd a = f < e ? f : e, bb = f < e ? e : f;
+    if (!(bb > a)) {
+      g[p] = img[p];
+      continue;
+    }
+    const qd d = bb - a, t0 = ((qd)theta[p] - a) / d, lam = d * d / (2 * (qd)sigma[p] * (qd)sigma[p]);
+    qd I[2];
+    integrals_q(lam, t0, 1, I, 0);
+    g[p] = (double)(a + d * (I[1] / I[0]));
+  }
+  free(vals);
+  return 0;
+}

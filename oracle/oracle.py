@@ -54,7 +54,9 @@ def _load():
             lib.fabfo_fit.argtypes = [P, i, P]
             lib.fabfo_stretch.argtypes = [P, i, d, d, P]
             lib.fabfo_integrals.argtypes = [d, d, i, P, i]
-            for fn in ("fabfo_bounds", "fabfo_brute", "fabfo_fast", "fabfo_window",
+            lib.fabfo_literal.argtypes = [P, P, P, i, i, i, i, i, P]
+            lib.fabfo_mozerov.argtypes = [P, P, P, i, i, i, i, l, l, P]
+            for fn in ("fabfo_bounds", "fabfo_brute", "fabfo_fast", "fabfo_window", "fabfo_literal", "fabfo_mozerov",
                        "fabfo_hilbert_inverse", "fabfo_fit", "fabfo_stretch", "fabfo_integrals"):
                 getattr(lib, fn).restype = ctypes.c_int
             _lib = lib
@@ -217,3 +219,40 @@ def integrals(lam: float, t0: float, K: int, method: int = 0):
     if used < 0:
         raise ValueError("bad arguments")
     return o, used
+
+
+def literal(img, theta, sigma, rho: int, N: int, threads: int | None = None):
+    """O3: Algorithm 1 as printed, plain fp64, the paper's [0,1] scaling,
+    running-sum box moments, eq.(24), eq.(19), eqs.(30)-(32) for every lambda, no
+    guard.  CONTEXT ONLY (not a parity target): how far the paper's own numerics
+    drift from ``fast``.  Whole images; images of a batch run in parallel."""
+    lib = _load()
+    f, th, sg = _as3d(img), _as3d(theta), _as3d(sigma)
+    B, H, W = f.shape
+    g = np.empty(f.shape, np.float64)
+
+    def run(b0, b1):
+        for b in range(b0, b1):
+            if lib.fabfo_literal(_ptr(f[b:b + 1]), _ptr(th[b:b + 1]), _ptr(sg[b:b + 1]), 1, H, W, rho, N,
+                                 _ptr(g[b:b + 1])):
+                raise ValueError("fabfo_literal: invalid arguments")
+
+    _parallel(B, run, threads, chunk=1)
+    return g.reshape(np.shape(img))
+
+
+def mozerov(img, theta, sigma, rho: int, threads: int | None = None):
+    """Mozerov & van de Weijer's uniform-prior filter as the paper compares it
+    (P:128-141): eq.(29) at N = 0 on [f, 2 fbar - f] (Delta = 0) instead of
+    [alpha, beta]; f where that interval is a point.  __float128 -> float64."""
+    lib = _load()
+    f, th, sg = _as3d(img), _as3d(theta), _as3d(sigma)
+    B, H, W = f.shape
+    g = np.empty(f.shape, np.float64)
+
+    def run(p0, p1):
+        if lib.fabfo_mozerov(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, p0, p1, _ptr(g)):
+            raise ValueError("fabfo_mozerov: invalid arguments")
+
+    _parallel(f.size, run, threads, chunk=2048)
+    return g.reshape(np.shape(img))

@@ -14,6 +14,8 @@ from .fabf import (  # noqa: F401
     filter_diag,
     filter_events,
     filter_host,
+    filter_interleaved,
+    filter_mozerov,
     filter_profile,
     lib,
     library_path,

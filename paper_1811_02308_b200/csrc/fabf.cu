@@ -1310,6 +1310,95 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
 }
 
 // ============================================================================
+// Mozerov & van de Weijer's uniform-prior filter (NEXT-4), the baseline the
+// paper compares with (Fig.3): a degree-0 fit of the local
+// histogram on [f(i), 2 fbar(i) - f(i)] (Delta = 0) instead of [alpha, beta],
+// i.e. eq.(29) at N = 0 on that interval (identity when it is a point).  One
+// CTA per T x T output tile: the (T + 2 rho)^2 footprint staged in shared
+// memory (reflected borders), box sums by sliding windows in fp64 (rows, then
+// columns), then the N = 0 integrals of fabf_device.cuh per pixel.
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_mozerov(const float* __restrict__ img,
+                                                       const float* __restrict__ theta,
+                                                       const float* __restrict__ sigma, float* __restrict__ out,
+                                                       int H, int W, int rho, unsigned flags) {
+  extern __shared__ __align__(16) unsigned char smm[];
+  const int w = 2 * rho + 1, FS = T + 2 * rho;
+  double* Hs = reinterpret_cast<double*>(smm);                       // [FS][T]
+  float* F = reinterpret_cast<float*>(smm + sizeof(double) * FS * T);  // [FS][FS]
+  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T, b = blockIdx.z;
+  const size_t plane = (size_t)b * H * W;
+  const float* src = img + plane;
+  for (int t = threadIdx.x; t < FS * FS; t += kThreads) {
+    const int r = t / FS, cc = t - r * FS;
+    F[t] = __ldg(src + (size_t)reflect_index(y0 - rho + r, H) * W + reflect_index(x0 - rho + cc, W));
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < FS; r += kThreads) {  // horizontal window sums, sliding
+    const float* Fr = F + r * FS;
+    double acc = 0.0;
+    for (int cc = 0; cc < w; ++cc) acc += Fr[cc];
+    Hs[r * T] = acc;
+    for (int x = 1; x < T; ++x) {
+      acc += (double)Fr[x + w - 1] - (double)Fr[x - 1];
+      Hs[r * T + x] = acc;
+    }
+  }
+  __syncthreads();
+  constexpr int SEG = T * T / kThreads;  // output rows per thread (column x, rows r0 .. r0 + SEG)
+  const int x = threadIdx.x % T, r0 = (threadIdx.x / T) * SEG;
+  double acc = 0.0;
+  for (int dy = 0; dy < w; ++dy) acc += Hs[(r0 + dy) * T + x];
+  const float n = (float)(w * w);
+  for (int k = 0; k < SEG; ++k) {
+    if (k > 0) acc += Hs[(r0 + k + w - 1) * T + x] - Hs[(r0 + k - 1) * T + x];
+    const int yy = y0 + r0 + k, xx = x0 + x;
+    if (yy >= H || xx >= W) continue;
+    const size_t o = plane + (size_t)yy * W + xx;
+    const double f = (double)F[(r0 + k + rho) * FS + x + rho];
+    const double e = 2.0 * (acc / (double)n) - f;  // 2 fbar - f
+    const float a = (float)fmin(f, e), bb = (float)fmax(f, e);
+    if (!(bb > a)) {
+      out[o] = (float)f;
+      continue;
+    }
+    const float th = theta[o], sg = sigma[o];
+    float lam, t0;
+    const int regime = range_params(a, bb, th, sg, lam, t0);
+    const PixelResult res = ghat_from_record<0>(nullptr, 1, th, sg, a, bb, regime, flags & kFlagLiteral, false, n);
+    out[o] = res.g;
+  }
+}
+
+// ============================================================================
+// colour (NEXT-3): channel-interleaved images (B x H x W x C) <-> the planar
+// batch (B C) x H x W the filter runs on, channel by channel as the paper
+// filters colour images.  Pure data movement, coalesced on the
+// interleaved side.
+__global__ void __launch_bounds__(kThreads) k_deinterleave(const float* __restrict__ a,
+                                                            const float* __restrict__ b,
+                                                            const float* __restrict__ c, float* __restrict__ pa,
+                                                            float* __restrict__ pb, float* __restrict__ pc,
+                                                            long long HW, int C, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long px = t / C, ch = t - px * C, bi = px / HW, q = px - bi * HW;
+    const long long o = (bi * C + ch) * HW + q;  // plane (b, ch), pixel q
+    pa[o] = a[t];
+    pb[o] = b[t];
+    pc[o] = c[t];
+  }
+}
+__global__ void __launch_bounds__(kThreads) k_interleave(const float* __restrict__ p, float* __restrict__ out,
+                                                          long long HW, int C, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long px = t / C, ch = t - px * C, bi = px / HW, q = px - bi * HW;
+    out[t] = p[(bi * C + ch) * HW + q];
+  }
+}
+
+// ============================================================================
 // FABF_FLAG_DEBUG: device-side check of the preconditions (include/fabf.h):
 // f, theta finite, sigma finite and > 0.  Counts violations of the pixels
 // [lo, lo + n) of each image b0 .. b0 + nb - 1 and keeps the smallest index.
@@ -1722,6 +1811,10 @@ cudaError_t alloc_ring(Plan* p) {
   return cudaMalloc(&p->ring, sizeof(float2) * (size_t)p->ring_elems);
 }
 
+// planar staging buffers (fabf_filter_host, fabf_filter_interleaved): three
+// planes of px floats, each starting 16-byte aligned
+size_t staging_pitch(size_t px) { return (px + 3) & ~(size_t)3; }
+
 // a fresh set of fallback counters per call
 fabf_status_t fallback_reset(Plan* p, int slots, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int) * (size_t)slots, st), "cudaMemsetAsync(fb_count)");
@@ -1843,7 +1936,8 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   const size_t px = (size_t)p->B * p->H * p->W, bytes = px * sizeof(float);
   if (!p->h_in) {
     cudaError_t e;
-    if ((e = cudaMalloc(&p->h_in, 3 * bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+    if ((e = cudaMalloc(&p->h_in, 3 * sizeof(float) * staging_pitch(px))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(staging)");
     if ((e = cudaMalloc(&p->h_out, bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
   }
   if (!p->cs_in) {
@@ -1860,8 +1954,8 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
     ~Record() { p->launches = g_launches; }
   } rec{p};
   float* dimg = p->h_in;
-  float* dth = p->h_in + px;
-  float* dsg = p->h_in + 2 * px;
+  float* dth = p->h_in + staging_pitch(px);
+  float* dsg = p->h_in + 2 * staging_pitch(px);
   fabf_status_t s = validate_filter(p, dimg, dth, dsg, rho, N, p->h_out);
   if (s != FABF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1918,6 +2012,76 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   }
   FABF_CUDA(cudaStreamSynchronize(p->cs_out), "cudaStreamSynchronize");
   FABF_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  return FABF_OK;
+}
+
+fabf_status_t fabf_filter_mozerov(fabf_plan_t plan, const float* img, const float* theta,
+                                  const float* sigma, int rho, float* out, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  fabf_status_t s = validate_filter(p, img, theta, sigma, rho, 0, out);
+  if (s != FABF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool small = 32 + 2 * rho <= 128;  // 32 x 32 tiles up to rho = 48, else 16 x 16
+  const int T = small ? 32 : 16, FS = T + 2 * rho;
+  const size_t smem = sizeof(double) * FS * T + sizeof(float) * FS * FS;
+  if (smem > (size_t)kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for shared memory");
+  {
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[p->device]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_mozerov<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_mozerov)");
+      FABF_CUDA(cudaFuncSetAttribute(k_mozerov<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_mozerov)");
+      attr_set[p->device] = true;
+    }
+  }
+  dim3 g((p->W + T - 1) / T, (p->H + T - 1) / T, p->B);
+  if (small)
+    k_mozerov<32><<<g, kThreads, smem, st>>>(img, theta, sigma, out, p->H, p->W, rho, p->flags);
+  else
+    k_mozerov<16><<<g, kThreads, smem, st>>>(img, theta, sigma, out, p->H, p->W, rho, p->flags);
+  FABF_CUDA(cudaGetLastError(), "k_mozerov launch");
+  p->launches = 1;
+  p->last_stream = st;
+  return FABF_OK;
+}
+
+fabf_status_t fabf_filter_interleaved(fabf_plan_t plan, const float* img, const float* theta,
+                                      const float* sigma, int channels, int rho, int N, float* out,
+                                      void* stream) {
+  // colour / multi-channel: the plan's batch counts planes, B = images x
+  // channels; inputs and output are B/C x H x W x C interleaved device buffers
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  if (!p) return fail(FABF_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (channels < 1 || p->B % channels != 0)
+    return fail(FABF_ERR_INVALID_ARGUMENT, "channels must divide the plan's batch (images x channels)");
+  if (!img || !theta || !sigma || !out) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  {
+    fabf_status_t s0 = check_plan_device(p);
+    if (s0 != FABF_OK) return s0;
+  }
+  const size_t px = (size_t)p->B * p->H * p->W, bytes = px * sizeof(float);
+  if (overlaps(out, bytes, img, bytes) || overlaps(out, bytes, theta, bytes) || overlaps(out, bytes, sigma, bytes))
+    return fail(FABF_ERR_INVALID_ARGUMENT, "out overlaps an input");
+  if (!p->h_in) {  // planar staging (shared with fabf_filter_host), allocated on first use
+    cudaError_t e;
+    if ((e = cudaMalloc(&p->h_in, 3 * sizeof(float) * staging_pitch(px))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(staging)");
+    if ((e = cudaMalloc(&p->h_out, bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long HW = (long long)p->H * p->W, total = (long long)px;
+  const int grid = (int)std::min<long long>(148LL * 8, (total + kThreads - 1) / kThreads);
+  const size_t pxp = staging_pitch(px);
+  k_deinterleave<<<grid, kThreads, 0, st>>>(img, theta, sigma, p->h_in, p->h_in + pxp, p->h_in + 2 * pxp, HW,
+                                             channels, total);
+  FABF_CUDA(cudaGetLastError(), "k_deinterleave launch");
+  fabf_status_t s = filter_impl(p, p->h_in, p->h_in + pxp, p->h_in + 2 * pxp, rho, N, p->h_out, nullptr, st);
+  if (s != FABF_OK) return s;
+  k_interleave<<<grid, kThreads, 0, st>>>(p->h_out, out, HW, channels, total);
+  FABF_CUDA(cudaGetLastError(), "k_interleave launch");
+  p->launches += 2;  // (filter_impl recorded its own kernels)
   return FABF_OK;
 }
 

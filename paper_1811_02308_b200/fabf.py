@@ -61,6 +61,12 @@ def lib():
             L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
             L.fabf_filter_events.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_void_p)]
             L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
+            if hasattr(L, "fabf_filter_mozerov"):
+                L.fabf_filter_mozerov.argtypes = [P, P, P, P, i, P, P]
+                L.fabf_filter_mozerov.restype = ctypes.c_int
+            if hasattr(L, "fabf_filter_interleaved"):
+                L.fabf_filter_interleaved.argtypes = [P, P, P, P, i, i, i, P, P]
+                L.fabf_filter_interleaved.restype = ctypes.c_int
             if hasattr(L, "fabf_last_launch_count"):  # (absent from round-1 builds kept for A/B timing)
                 L.fabf_last_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
                 L.fabf_last_launch_count.restype = ctypes.c_int
@@ -259,3 +265,40 @@ def filter_profile(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, st
                                      _dev_ptr(sigma, "sigma", plan), int(rho), int(N), _dev_ptr(out, "out", plan),
                                      _stream_ptr(stream), ms))
     return out, [float(v) for v in ms]
+
+
+def filter_interleaved(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=None):
+    """fabf_filter_interleaved: colour / multi-channel images filtered channel by
+    channel.  ``img``, ``theta``, ``sigma``: contiguous float32 CUDA
+    tensors of shape (H, W, C) or (B, H, W, C); the plan's batch must be B * C
+    planes.  Returns ``out`` (same shape)."""
+    import torch
+
+    if img.dim() not in (3, 4):
+        raise FabfError(1, "img must be (H, W, C) or (B, H, W, C)")
+    C = int(img.shape[-1])
+    if out is None:
+        out = torch.empty_like(img)
+
+    def ptr(t, name):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+            raise FabfError(1, f"{name} must be a contiguous float32 CUDA tensor")
+        if t.shape != img.shape or t.numel() != _numel(plan.shape):
+            raise FabfError(1, f"{name} must have the image's shape and the plan's pixel count")
+        return ctypes.c_void_p(t.data_ptr())
+
+    _check(lib().fabf_filter_interleaved(plan.handle, ptr(img, "img"), ptr(theta, "theta"), ptr(sigma, "sigma"),
+                                         C, int(rho), int(N), ptr(out, "out"), _stream_ptr(stream)))
+    return out
+
+
+def filter_mozerov(plan: Plan, img, theta, sigma, rho: int, out=None, stream=None):
+    """fabf_filter_mozerov: the uniform-prior baseline on device tensors."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(img)
+    _check(lib().fabf_filter_mozerov(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
+                                     _dev_ptr(sigma, "sigma", plan), int(rho), _dev_ptr(out, "out", plan),
+                                     _stream_ptr(stream)))
+    return out

@@ -472,3 +472,54 @@ def test_psnr_against_brute_force_config1(fb, orc):
     out, _, _ = _run(fb, w)
     g = orc.brute(w.img, w.theta, w.sigma, w.rho)
     assert psnr(out, g) > 40.0  # the paper's acceptance bar
+
+
+@pytest.mark.parametrize("B,H,W,C,rho,N", [(2, 96, 130, 3, 5, 6), (1, 120, 200, 3, 12, 8), (1, 37, 53, 3, 3, 5),
+                                           (1, 64, 64, 4, 2, 4)])
+def test_colour_interleaved_channel_by_channel(fb, orc, B, H, W, C, rho, N):
+    """NEXT-3 colour (channel by channel): fabf_filter_interleaved on
+    B x H x W x C interleaved buffers equals the oracle applied to each channel
+    plane (different content per channel); odd pixel counts included."""
+    import torch
+
+    rng = np.random.default_rng(B * 1000 + H + C)
+    kinds = ["rect", "texture", "voronoi", "float"]
+    planes = [workloads.random_case(B, H, W, seed=40 + ch, kind=kinds[ch % 4], rho=rho, N=N) for ch in range(C)]
+    img = np.stack([p.img for p in planes], axis=-1).astype(np.float32)
+    th = np.stack([p.theta for p in planes], axis=-1).astype(np.float32)
+    sg = np.stack([p.sigma for p in planes], axis=-1).astype(np.float32)
+    plan = fb.Plan(B * C, H, W)
+    out = fb.filter_interleaved(plan, _dev(img), _dev(th), _dev(sg), rho, N)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy()
+    assert out.shape == img.shape
+    for ch in range(C):
+        o = orc.fast(img[..., ch], th[..., ch], sg[..., ch], rho, N)
+        mx, nbad, _ = compare_guarded(out[..., ch], o, grey_scale(img[..., ch]))
+        assert nbad == 0, f"channel {ch}: max |delta| = {mx}"
+    with pytest.raises(fb.FabfError):
+        fb.filter_interleaved(fb.Plan(B * C + 1, H, W), _dev(img), _dev(th), _dev(sg), rho, N)
+
+
+@pytest.mark.parametrize("kind,shape,rho", [("cfg1", None, 3), ("cfg2", None, 5), ("rect", (2, 70, 91), 10),
+                                            ("float", (1, 57, 91), 3), ("flat", (1, 40, 40), 2),
+                                            ("texture", (1, 150, 140), 60)])
+def test_mozerov_baseline(fb, orc, kind, shape, rho):
+    """NEXT-4: fabf_filter_mozerov (eq.(29) at N = 0 on [f, 2 fbar - f])
+    against the oracle's __float128 version, every pixel (the rho = 60 case
+    runs the 16 x 16 tile variant)."""
+    import torch
+
+    if kind == "cfg1":
+        w = workloads.config(1)
+    elif kind == "cfg2":
+        w = workloads.config(2)
+    else:
+        w = workloads.random_case(*shape, seed=19, kind=kind, rho=rho, N=0)
+    plan = fb.Plan(*w.shape)
+    out = fb.filter_mozerov(plan, _dev(w.img), _dev(w.theta), _dev(w.sigma), rho)
+    torch.cuda.synchronize()
+    ref = orc.mozerov(w.img, w.theta, w.sigma, rho)
+    sc = grey_scale(w.img)
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref) / sc
+    assert err.max() <= TOL_GREY, f"max |delta| = {err.max()} grey"

@@ -408,3 +408,47 @@ def test_histogram_route_equals_sample_sums(orc, kind):
         b = orc.fast_window(vals, vals[n // 2], theta, sigma, N, route=1)
         for k in ("g_lit", "g_guard", "kappa", "t2n"):
             assert a[k] == pytest.approx(b[k], rel=1e-13, abs=1e-13), (trial, k)
+
+
+def test_literal_o3_matches_reference_when_well_conditioned(orc):
+    """O3 (Algorithm 1 as printed, fp64, context only) equals the __float128
+    reference where the paper's numerics are safe: small N, lambda >= 2 (forward
+    recursion stable), no guard firing.  A dropped term in eq.(24), eq.(19),
+    eq.(30)-(32) or the [0,1] scaling would show up here."""
+    w = workloads.random_case(1, 40, 48, seed=21, kind="rect", rho=3, N=3)
+    sg = np.full_like(w.sigma, 12.0)
+    lit = orc.literal(w.img, w.theta, sg, 3, 3)
+    o = orc.fast(w.img, w.theta, sg, 3, 3)
+    ok = (o["kappa"] < 50) & (o["code"] & orc.CODE_QUAD == 0)
+    assert ok.mean() > 0.5
+    assert np.max(np.abs(lit[ok] - o["g_lit"][ok])) < 1e-6
+    ident = (o["code"] & orc.CODE_IDENTITY) > 0
+    assert np.array_equal(lit[ident], w.img[ident].astype(np.float64))
+
+
+def test_mozerov_against_quadrature_and_limits(orc):
+    """The Mozerov baseline: the range-kernel-weighted mean of a uniform
+    density on [f, 2 fbar - f], evaluated here by mpmath quadrature of that ratio
+    (no erf, no recursion); sigma -> inf gives the interval's midpoint = fbar; a
+    constant image maps to itself."""
+    import mpmath as mp
+
+    w = workloads.random_case(1, 15, 17, seed=33, kind="rect", rho=2, N=0)
+    g = orc.mozerov(w.img, w.theta, w.sigma, 2)
+    f = w.img[0]
+    pad = np.pad(f.astype(np.float64), 2, mode="symmetric")
+    for (y, x) in [(0, 0), (7, 8), (14, 16), (3, 12), (10, 1)]:
+        fbar = pad[y:y + 5, x:x + 5].mean()
+        a, b = sorted((float(f[y, x]), 2 * fbar - float(f[y, x])))
+        th, s = float(w.theta[0, y, x]), float(w.sigma[0, y, x])
+        if b - a < 1e-9:
+            assert g[0, y, x] == f[y, x]
+            continue
+        k = lambda t: mp.exp(-(t - th) ** 2 / (2 * s * s))
+        ref = mp.quad(lambda t: t * k(t), [a, b]) / mp.quad(k, [a, b])
+        assert g[0, y, x] == pytest.approx(float(ref), abs=1e-9)
+    big = orc.mozerov(w.img, w.theta, np.full_like(w.sigma, 1e7), 2)
+    box = np.array([[pad[y:y + 5, x:x + 5].mean() for x in range(17)] for y in range(15)])
+    assert np.max(np.abs(big[0] - box)) < 1e-6
+    c = np.full((1, 9, 9), 77.0, np.float32)
+    assert np.all(orc.mozerov(c, c + 3, np.full_like(c, 10.0), 2) == 77.0)
