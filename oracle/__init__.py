@@ -17,6 +17,8 @@ from .oracle import (  # noqa: F401
     integrals,
     literal,
     mozerov,
+    sharpen_maps,
+    SHARPEN_DEFAULTS,
     stretch,
     CODE_IDENTITY,
     CODE_GUARD,

@@ -651,3 +651,50 @@ int fabfo_mozerov(const float* img, const float* theta, const float* sigma, int 
   free(vals);
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-2: the sharpening / denoising application's range-kernel maps,        */
+/* P:620-630 (after Zhang & Allebach):                                         */
+/*   theta(i) = f(i) + zeta(i),  zeta(i) = f(i) - fbar(i)                      */
+/*              (fbar = average over the Omega neighbourhood: the box of       */
+/*              half-width rho, reading R1);                                   */
+/*   sigma(i) = an affine map of |LoG f|(i) that maps low values to high sigma:*/
+/*              sigma = s_hi - (s_hi - s_lo) min(|L(i)| / l_sat, 1)            */
+/*              (the paper gives neither the LoG scale nor the map; reading    */
+/*              R15: these four parameters are inputs);                        */
+/*   L = Laplacian of Gaussian at scale s: the sampled, normalised Gaussian    */
+/*       g(x) ~ exp(-x^2 / 2s^2) on |x| <= ceil(4 s) and its second derivative */
+/*       g''(x) = (x^2 - s^2) / s^4 g(x); L(i) = sum_{dy,dx} [g''(dx) g(dy) +  */
+/*       g(dx) g''(dy)] f(i - (dy, dx)), borders reflected (reading R2).        */
+/* Direct sums in fp64 (__float128 for fbar), pixel by pixel.                 */
+int fabfo_sharpen_maps(const float* img, int B, int H, int W, int rho, double s, double s_lo, double s_hi,
+                       double l_sat, long p0, long p1, double* theta, double* sigma) {
+  if (!img || !theta || !sigma || B < 1 || H < 1 || W < 1 || rho < 0 || !(s > 0) || !(l_sat > 0)) return 1;
+  const int r = (int)ceil(4.0 * s);
+  if (2 * rho + 1 > H || 2 * rho + 1 > W || 2 * r + 1 > H || 2 * r + 1 > W || r > 64) return 1;
+  const long HW = (long)H * W;
+  double g[129], g2[129], gs = 0;
+  for (int k = -r; k <= r; ++k) gs += (g[k + r] = exp(-0.5 * k * k / (s * s)));
+  for (int k = -r; k <= r; ++k) {
+    g[k + r] /= gs;
+    g2[k + r] = ((double)k * k - s * s) / (s * s * s * s) * g[k + r];
+  }
+  const int n = (2 * rho + 1) * (2 * rho + 1);
+  for (long p = p0; p < p1; ++p) {
+    const long b = p / HW, rr = p % HW, y = rr / W, x = rr % W;
+    const float* base = img + b * HW;
+    qd acc = 0;
+    for (long dy = -rho; dy <= rho; ++dy)
+      for (long dx = -rho; dx <= rho; ++dx) acc += base[reflect_index(y + dy, H) * W + reflect_index(x + dx, W)];
+    const double fbar = (double)(acc / n), f = base[y * W + x];
+    theta[p] = f + (f - fbar);
+    double L = 0;
+    for (int dy = -r; dy <= r; ++dy)
+      for (int dx = -r; dx <= r; ++dx)
+        L += (g2[dx + r] * g[dy + r] + g[dx + r] * g2[dy + r]) *
+             base[reflect_index(y - dy, H) * W + reflect_index(x - dx, W)];
+    const double u = fabs(L) / l_sat;
+    sigma[p] = s_hi - (s_hi - s_lo) * (u < 1.0 ? u : 1.0);
+  }
+  return 0;
+}

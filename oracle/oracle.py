@@ -56,7 +56,9 @@ def _load():
             lib.fabfo_integrals.argtypes = [d, d, i, P, i]
             lib.fabfo_literal.argtypes = [P, P, P, i, i, i, i, i, P]
             lib.fabfo_mozerov.argtypes = [P, P, P, i, i, i, i, l, l, P]
+            lib.fabfo_sharpen_maps.argtypes = [P, i, i, i, i, d, d, d, d, l, l, P, P]
             for fn in ("fabfo_bounds", "fabfo_brute", "fabfo_fast", "fabfo_window", "fabfo_literal", "fabfo_mozerov",
+                       "fabfo_sharpen_maps",
                        "fabfo_hilbert_inverse", "fabfo_fit", "fabfo_stretch", "fabfo_integrals"):
                 getattr(lib, fn).restype = ctypes.c_int
             _lib = lib
@@ -256,3 +258,26 @@ def mozerov(img, theta, sigma, rho: int, threads: int | None = None):
 
     _parallel(f.size, run, threads, chunk=2048)
     return g.reshape(np.shape(img))
+
+
+SHARPEN_DEFAULTS = dict(log_scale=1.0, sigma_lo=10.0, sigma_hi=40.0, log_sat=20.0)
+
+
+def sharpen_maps(img, rho: int, log_scale=1.0, sigma_lo=10.0, sigma_hi=40.0, log_sat=20.0,
+                 threads: int | None = None):
+    """The sharpening application's maps: theta = 2f - fbar (box mean
+    over Omega), sigma = sigma_hi - (sigma_hi - sigma_lo) min(|LoG f| / log_sat, 1)
+    (reading R15).  Returns (theta, sigma) as float64."""
+    lib = _load()
+    f = _as3d(img)
+    B, H, W = f.shape
+    th = np.empty(f.shape, np.float64)
+    sg = np.empty(f.shape, np.float64)
+
+    def run(p0, p1):
+        if lib.fabfo_sharpen_maps(_ptr(f), B, H, W, rho, float(log_scale), float(sigma_lo), float(sigma_hi),
+                                  float(log_sat), p0, p1, _ptr(th), _ptr(sg)):
+            raise ValueError("fabfo_sharpen_maps: invalid arguments")
+
+    _parallel(f.size, run, threads, chunk=4096)
+    return th.reshape(np.shape(img)), sg.reshape(np.shape(img))

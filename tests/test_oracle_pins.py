@@ -452,3 +452,21 @@ def test_mozerov_against_quadrature_and_limits(orc):
     assert np.max(np.abs(big[0] - box)) < 1e-6
     c = np.full((1, 9, 9), 77.0, np.float32)
     assert np.all(orc.mozerov(c, c + 3, np.full_like(c, 10.0), 2) == 77.0)
+
+
+@pytest.mark.parametrize("rho,s", [(5, 1.0), (2, 0.7), (3, 2.0)])
+def test_sharpen_maps_against_scipy(orc, rho, s):
+    """P:620-630 maps: fbar equals scipy's uniform_filter and the LoG equals
+    scipy's gaussian_laplace (reflect borders, truncate 4) -- independent
+    library routines; sigma is the stated affine map of |LoG|, clipped."""
+    from scipy import ndimage
+
+    w = workloads.random_case(1, 33, 41, seed=61, kind="texture", rho=rho, N=0)
+    f = w.img[0].astype(np.float64)
+    th, sg = orc.sharpen_maps(w.img, rho, log_scale=s, sigma_lo=8.0, sigma_hi=35.0, log_sat=12.0)
+    fbar = ndimage.uniform_filter(f, size=2 * rho + 1, mode="reflect")
+    assert np.max(np.abs(th[0] - (2 * f - fbar))) < 1e-9
+    L = ndimage.gaussian_laplace(f, s, mode="reflect", truncate=4.0)
+    ref = 35.0 - (35.0 - 8.0) * np.minimum(np.abs(L) / 12.0, 1.0)
+    assert np.max(np.abs(sg[0] - ref)) < 1e-9
+    assert sg.min() >= 8.0 and sg.max() <= 35.0
