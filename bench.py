@@ -312,6 +312,7 @@ def run_gpu(args):
     mix = regime_mix(fb, plan, img, th, sg, w.rho, w.N)  # outside the timed region
     fused = {} if args.no_other_configs else fused_variant(fb, w, img, th, sg, flush)
     colour = {} if args.no_other_configs else colour_variant(fb, dev, flush)
+    sharpen = {} if args.no_other_configs else sharpen_variant(fb, dev, flush)
     others = {} if args.no_other_configs else other_configs(fb, dev, flush)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
@@ -381,6 +382,7 @@ def run_gpu(args):
             "other_configs": others,
             "fused_variant": fused,
             "colour_variant": colour,
+            "sharpen_variant": sharpen,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
@@ -487,6 +489,51 @@ def colour_variant(fb, dev, flush, steps: int = 10):
     ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
     return {"workload": "3840x2160x3 interleaved RGB, rho=20, N=8", "colour Mpix/s": H * W / (ms * 1e-3) / 1e6,
             "plane Mpix/s": C * H * W / (ms * 1e-3) / 1e6, "ms_per_frame": ms, "launches": plan.last_launch_count()}
+
+
+def sharpen_variant(fb, dev, flush, steps: int = 10):
+    """NEXT-2: the sharpening application at the paper's Fig.4 size
+    (1024x1024, rho = 5, N = 5; synthetic Voronoi + noise stand-in) and at 4K
+    (rho = 20, N = 8): theta, sigma produced on the device from f alone
+    (fabf_filter_sharpen).  Device-timed Mpix/s, and end to end with the
+    pinned-host image uploaded and the result read back every frame (4 + 4
+    bytes per pixel instead of 12 + 4)."""
+    import torch
+
+    import workloads
+
+    res = {}
+    for name, (H, W, rho, N) in {"sharpen_1024_rho5_N5": (1024, 1024, 5, 5),
+                                 "sharpen_4k_rho20_N8": (2160, 3840, 20, 8)}.items():
+        f = workloads.voronoi(H, W, seed=7000 + H, n_seeds=128, noise_sd=12.0).astype(np.float32)[None]
+        img = torch.from_numpy(f).to(dev)
+        out = torch.empty_like(img)
+        plan = fb.Plan(1, H, W)
+        stream = torch.cuda.current_stream()
+        for _ in range(3):
+            fb.filter_sharpen(plan, img, rho, N, out=out)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in ev:
+            flush.fill_(1.0)
+            a.record(stream)
+            fb.filter_sharpen(plan, img, rho, N, out=out)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        h_img = torch.from_numpy(f).pin_memory()
+        h_out = torch.empty_like(h_img).pin_memory()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            img.copy_(h_img, non_blocking=True)
+            fb.filter_sharpen(plan, img, rho, N, out=out)
+            h_out.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_s = (time.perf_counter() - t0) / steps
+        res[name] = {"Mpix/s": H * W / (ms * 1e-3) / 1e6, "ms": ms, "launches": plan.last_launch_count(),
+                     "e2e Mpix/s": H * W / e2e_s / 1e6, "e2e_ms": e2e_s * 1e3,
+                     "h2d_bytes_per_frame": 4 * H * W, "d2h_bytes_per_frame": 4 * H * W,
+                     "params": dict(fb.SHARPEN_DEFAULTS)}
+    return res
 
 
 def run_sweep(args):

@@ -128,6 +128,34 @@ fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* al
 fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
                                const float* sigma, int rho, int N, float* out, void* stream);
 
+/* NEXT-2: the sharpening / noise-removal application (after Zhang &
+ * Allebach): the range-kernel maps are produced on the device from f alone,
+ *   theta(i) = f(i) + zeta(i), zeta = f - fbar (fbar: box mean over the same
+ *              (2 rho + 1)^2 window Omega),
+ *   sigma(i) = sigma_hi - (sigma_hi - sigma_lo) min(|LoG f|(i) / log_sat, 1)
+ * (the paper says only "an affine mapping on the absolute value" of the LoG
+ * response that maps low values to high sigma: the LoG scale and the map are
+ * parameters, reading R15).  LoG: the sampled, normalised Gaussian of
+ * std log_scale on |x| <= ceil(4 log_scale) (<= 16) and its analytic second
+ * derivative, borders reflected.                                              */
+typedef struct {
+  float log_scale; /* LoG Gaussian std (pixels)                    */
+  float sigma_lo;  /* sigma where |LoG| >= log_sat (edges)         */
+  float sigma_hi;  /* sigma where LoG = 0 (flat areas)             */
+  float log_sat;   /* |LoG| (intensity units) at which sigma_lo is reached */
+} fabf_sharpen_t;
+
+/* The maps alone: theta, sigma (device, batch x height x width fp32) from img.
+ * Asynchronous.  INVALID_ARGUMENT for bad parameters or overlapping buffers.   */
+fabf_status_t fabf_sharpen_maps(fabf_plan_t plan, const float* img, int rho, const fabf_sharpen_t* prm,
+                                float* theta, float* sigma, void* stream);
+
+/* The whole application: the maps into plan-owned buffers (allocated on first
+ * use, shared with fabf_filter_host), then fabf_filter with them -- img and out
+ * are the only caller buffers (4 + 4 bytes per pixel cross PCIe end to end).  */
+fabf_status_t fabf_filter_sharpen(fabf_plan_t plan, const float* img, int rho, int N, const fabf_sharpen_t* prm,
+                                  float* out, void* stream);
+
 /* The baseline the paper compares with (NEXT-4): Mozerov & van de Weijer's
  * uniform-prior filter with Delta = 0 (Fig.3) -- eq.(29) at
  * N = 0 fitted on [f(i), 2 fbar(i) - f(i)] (fbar = the box mean over the same

@@ -123,17 +123,27 @@ int fabfo_bounds(const float* img, int B, int H, int W, int rho, long p0, long p
 /* eq.(1)-(3) P:54-67: brute-force adaptive bilateral filter, box omega.       */
 /* phi_i(t) = exp(-t^2 / (2 sigma(i)^2)); weights shifted by the smallest      */
 /* exponent in the window (common factor, cancels in the ratio).               */
-int fabfo_brute(const float* img, const float* theta, const float* sigma, int B,
-                int H, int W, int rho, long p0, long p1, double* g) {
+static int gauss_weights(int rho, double** w);
+static int brute_impl(const float* img, const float* theta, const float* sigma, int B,
+                      int H, int W, int rho, int gauss, long p0, long p1, double* g) {
   if (!img || !theta || !sigma || !g || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
-  if (2 * rho + 1 > H || 2 * rho + 1 > W) return 1;
+  double* wts = NULL;
+  const int R = gauss ? gauss_weights(rho, &wts) : rho;
+  if (R < 0) return 2;
+  if (2 * R + 1 > H || 2 * R + 1 > W) {
+    free(wts);
+    return 1;
+  }
   long HW = (long)H * W;
-  int n = (2 * rho + 1) * (2 * rho + 1);
+  int n = (2 * R + 1) * (2 * R + 1);
   float* vals = (float*)malloc(sizeof(float) * (size_t)n);
-  if (!vals) return 2;
+  if (!vals) {
+    free(wts);
+    return 2;
+  }
   for (long p = p0; p < p1; ++p) {
     long b = p / HW, r = p % HW, y = r / W, x = r % W;
-    gather_window(img, H, W, rho, b, y, x, vals);
+    gather_window(img, H, W, R, b, y, x, vals);
     double th = theta[p], s = sigma[p];
     double inv2s2 = 1.0 / (2.0 * s * s);
     double emin = INFINITY;
@@ -144,14 +154,26 @@ int fabfo_brute(const float* img, const float* theta, const float* sigma, int B,
     double num = 0.0, den = 0.0;
     for (int j = 0; j < n; ++j) {
       double e = ((double)vals[j] - th) * ((double)vals[j] - th) * inv2s2;
-      double w = exp(-(e - emin)); /* omega(j) = 1 (box) */
+      double w = exp(-(e - emin)) * (wts ? wts[j] : 1.0); /* omega(j): 1 (box) or eq.(4) */
       num += w * (double)vals[j];
       den += w;
     }
     g[p] = num / den;
   }
   free(vals);
+  free(wts);
   return 0;
+}
+
+int fabfo_brute(const float* img, const float* theta, const float* sigma, int B,
+                int H, int W, int rho, long p0, long p1, double* g) {
+  return brute_impl(img, theta, sigma, B, H, W, rho, 0, p0, p1, g);
+}
+
+/* eq.(1)-(3) with the Gaussian omega of eq.(4) on [-3 rho, 3 rho]^2 (NEXT-1)  */
+int fabfo_brute_gauss(const float* img, const float* theta, const float* sigma, int B,
+                      int H, int W, int rho, long p0, long p1, double* g) {
+  return brute_impl(img, theta, sigma, B, H, W, rho, 1, p0, p1, g);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -351,10 +373,29 @@ static void add_powers(qd t, qd count, int N, qd* mu) {
   }
 }
 
-static void stretched_moments(const float* vals, int n, float amin, float bmax, int N, int route,
-                              qd* mu) {
+static void stretched_moments(const float* vals, const double* wts, int n, float amin, float bmax, int N,
+                              int route, qd* mu) {
   const qd alpha = amin, d = (qd)bmax - (qd)amin;
   for (int k = 0; k <= N; ++k) mu[k] = 0;
+  if (wts) { /* weighted histogram h_i of eq.(5) with omega(j) = wts[j] (Gaussian omega, eq.(4)) */
+    if (route == 1) {
+      for (int j = 0; j < n; ++j) add_powers(((qd)vals[j] - alpha) / d, wts[j], N, mu);
+      return;
+    }
+    int integral = (double)bmax - (double)amin <= FABFO_HIST_SPAN;
+    for (int j = 0; j < n && integral; ++j) integral = vals[j] == floorf(vals[j]);
+    if (!integral) {
+      for (int j = 0; j < n; ++j) add_powers(((qd)vals[j] - alpha) / d, wts[j], N, mu);
+      return;
+    }
+    static __thread qd hw[FABFO_HIST_SPAN + 1];
+    const int span = (int)((double)bmax - (double)amin);
+    for (int v = 0; v <= span; ++v) hw[v] = 0;
+    for (int j = 0; j < n; ++j) hw[(int)((double)vals[j] - (double)amin)] += wts[j];
+    for (int v = 0; v <= span; ++v)
+      if (hw[v] != 0) add_powers((qd)v / d, hw[v], N, mu);
+    return;
+  }
   if (route == 1) {
     for (int j = 0; j < n; ++j) add_powers(((qd)vals[j] - alpha) / d, 1, N, mu);
     return;
@@ -399,8 +440,8 @@ typedef struct {
 } fabfo_px;
 
 /* Algorithm 1 P:446-477 for one pixel whose window samples are vals[0..n-1]  */
-static void fast_window(const float* vals, int n, float f_center, float theta, float sigma,
-                        int N, int route, fabfo_px* out) {
+static void fast_window(const float* vals, const double* wts, int n, float f_center, float theta,
+                        float sigma, int N, int route, fabfo_px* out) {
   memset(out, 0, sizeof(*out));
   float amin = vals[0], bmax = vals[0];
   for (int j = 1; j < n; ++j) {
@@ -418,7 +459,7 @@ static void fast_window(const float* vals, int n, float f_center, float theta, f
 
   /* eq.(22): mu_k = sum_{t in Gamma_i} t^k H_i(t) */
   qd mu[FABFO_MAX_N + 1];
-  stretched_moments(vals, n, amin, bmax, N, route, mu);
+  stretched_moments(vals, wts, n, amin, bmax, N, route, mu);
   /* line 11: c = A^{-1} mu */
   qd c[FABFO_MAX_N + 1];
   fit_q(mu, N, c);
@@ -457,7 +498,7 @@ static void fast_window(const float* vals, int n, float f_center, float theta, f
   out->g_lit = (double)g_lit;
   out->g_guard = (double)g_guard;
   out->kappa = (double)kappa;
-  out->t2n = (double)(T2 / n);
+  out->t2n = (double)(T2 / mu[0]); /* T2 / (sum of the weights) */
   out->lam = (double)lam;
   out->t0 = (double)t0;
   out->code = code;
@@ -469,7 +510,7 @@ int fabfo_window(const float* vals, int n, float f_center, float theta, float si
                  int route, double* out6, int* code) {
   if (!vals || n < 1 || N < 0 || N > FABFO_MAX_N || !out6 || route < 0 || route > 1) return 1;
   fabfo_px px;
-  fast_window(vals, n, f_center, theta, sigma, N, route, &px);
+  fast_window(vals, NULL, n, f_center, theta, sigma, N, route, &px);
   out6[0] = px.g_lit;
   out6[1] = px.g_guard;
   out6[2] = px.kappa;
@@ -483,25 +524,49 @@ int fabfo_window(const float* vals, int n, float f_center, float theta, float si
 /* whole-image (or pixel-list) driver.  Pixels are flat indices into B*H*W.
  * If idx is NULL the pixels are p0..p1-1, else idx[p0..p1-1].  Any output
  * pointer may be NULL.  Output arrays are indexed like the pixel list.        */
-int fabfo_fast(const float* img, const float* theta, const float* sigma, int B, int H, int W,
-               int rho, int N, const long* idx, long p0, long p1, double* g_lit,
-               double* g_guard, double* kappa, double* t2n, unsigned char* code) {
+/* NEXT-1: the paper's default spatial kernel, eq.(4): omega(j) =
+ * exp(-|j|^2 / 2 rho^2) on Omega = [-3 rho, 3 rho]^2 (the window "typically
+ * set").  Returns the window half-width R and fills w[(2R+1)^2] in the
+ * order gather_window produces the samples (dy outer, dx inner), or -1.      */
+static int gauss_weights(int rho, double** w) {
+  const int R = 3 * rho, side = 2 * R + 1;
+  *w = (double*)malloc(sizeof(double) * (size_t)side * side);
+  if (!*w) return -1;
+  for (int dy = -R; dy <= R; ++dy)
+    for (int dx = -R; dx <= R; ++dx)
+      (*w)[(dy + R) * side + dx + R] = rho > 0 ? exp(-(double)(dy * dy + dx * dx) / (2.0 * rho * rho)) : 1.0;
+  return R;
+}
+
+static int fast_impl(const float* img, const float* theta, const float* sigma, int B, int H, int W,
+                     int rho, int N, int gauss, const long* idx, long p0, long p1, double* g_lit,
+                     double* g_guard, double* kappa, double* t2n, unsigned char* code) {
   if (!img || !theta || !sigma || B < 1 || H < 1 || W < 1 || rho < 0) return 1;
-  if (2 * rho + 1 > H || 2 * rho + 1 > W || N < 0 || N > FABFO_MAX_N) return 1;
+  double* wts = NULL;
+  const int R = gauss ? gauss_weights(rho, &wts) : rho;
+  if (R < 0) return 2;
+  if (2 * R + 1 > H || 2 * R + 1 > W || N < 0 || N > FABFO_MAX_N) {
+    free(wts);
+    return 1;
+  }
   long HW = (long)H * W;
-  int n = (2 * rho + 1) * (2 * rho + 1);
+  int n = (2 * R + 1) * (2 * R + 1);
   float* vals = (float*)malloc(sizeof(float) * (size_t)n);
-  if (!vals) return 2;
+  if (!vals) {
+    free(wts);
+    return 2;
+  }
   for (long q = p0; q < p1; ++q) {
     long p = idx ? idx[q] : q;
     if (p < 0 || p >= (long)B * HW) {
       free(vals);
+      free(wts);
       return 1;
     }
     long b = p / HW, r = p % HW, y = r / W, x = r % W;
-    gather_window(img, H, W, rho, b, y, x, vals);
+    gather_window(img, H, W, R, b, y, x, vals);
     fabfo_px px;
-    fast_window(vals, n, img[p], theta[p], sigma[p], N, 0, &px);
+    fast_window(vals, wts, n, img[p], theta[p], sigma[p], N, 0, &px);
     if (g_lit) g_lit[q] = px.g_lit;
     if (g_guard) g_guard[q] = px.g_guard;
     if (kappa) kappa[q] = px.kappa;
@@ -509,6 +574,37 @@ int fabfo_fast(const float* img, const float* theta, const float* sigma, int B, 
     if (code) code[q] = (unsigned char)px.code;
   }
   free(vals);
+  free(wts);
+  return 0;
+}
+
+int fabfo_fast(const float* img, const float* theta, const float* sigma, int B, int H, int W,
+               int rho, int N, const long* idx, long p0, long p1, double* g_lit,
+               double* g_guard, double* kappa, double* t2n, unsigned char* code) {
+  return fast_impl(img, theta, sigma, B, H, W, rho, N, 0, idx, p0, p1, g_lit, g_guard, kappa, t2n, code);
+}
+
+/* Algorithm 1 with the Gaussian omega of eq.(4) on [-3 rho, 3 rho]^2 (NEXT-1):
+ * the weighted histogram of eq.(5), everything else as fabfo_fast.            */
+int fabfo_fast_gauss(const float* img, const float* theta, const float* sigma, int B, int H, int W,
+                     int rho, int N, const long* idx, long p0, long p1, double* g_lit,
+                     double* g_guard, double* kappa, double* t2n, unsigned char* code) {
+  return fast_impl(img, theta, sigma, B, H, W, rho, N, 1, idx, p0, p1, g_lit, g_guard, kappa, t2n, code);
+}
+
+/* one explicitly weighted window (pins of the Gaussian route): omega(j) = wts[j] */
+int fabfo_window_w(const float* vals, const double* wts, int n, float f_center, float theta, float sigma,
+                   int N, int route, double* out6, int* code) {
+  if (!vals || !wts || n < 1 || N < 0 || N > FABFO_MAX_N || !out6 || route < 0 || route > 1) return 1;
+  fabfo_px px;
+  fast_window(vals, wts, n, f_center, theta, sigma, N, route, &px);
+  out6[0] = px.g_lit;
+  out6[1] = px.g_guard;
+  out6[2] = px.kappa;
+  out6[3] = px.t2n;
+  out6[4] = px.lam;
+  out6[5] = px.t0;
+  if (code) *code = px.code;
   return 0;
 }
 

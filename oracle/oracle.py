@@ -56,9 +56,12 @@ def _load():
             lib.fabfo_integrals.argtypes = [d, d, i, P, i]
             lib.fabfo_literal.argtypes = [P, P, P, i, i, i, i, i, P]
             lib.fabfo_mozerov.argtypes = [P, P, P, i, i, i, i, l, l, P]
+            lib.fabfo_fast_gauss.argtypes = [P, P, P, i, i, i, i, i, P, l, l, P, P, P, P, P]
+            lib.fabfo_brute_gauss.argtypes = [P, P, P, i, i, i, i, l, l, P]
+            lib.fabfo_window_w.argtypes = [P, P, i, ctypes.c_float, ctypes.c_float, ctypes.c_float, i, i, P, P]
             lib.fabfo_sharpen_maps.argtypes = [P, i, i, i, i, d, d, d, d, l, l, P, P]
             for fn in ("fabfo_bounds", "fabfo_brute", "fabfo_fast", "fabfo_window", "fabfo_literal", "fabfo_mozerov",
-                       "fabfo_sharpen_maps",
+                       "fabfo_sharpen_maps", "fabfo_fast_gauss", "fabfo_brute_gauss", "fabfo_window_w",
                        "fabfo_hilbert_inverse", "fabfo_fit", "fabfo_stretch", "fabfo_integrals"):
                 getattr(lib, fn).restype = ctypes.c_int
             _lib = lib
@@ -111,22 +114,25 @@ def bounds(img, rho: int, threads: int | None = None):
     return alpha.reshape(shp), beta.reshape(shp)
 
 
-def brute(img, theta, sigma, rho: int, threads: int | None = None):
-    """eq.(1)-(3) P:54-67, box spatial kernel, fp64 -> g (float64)."""
+def brute(img, theta, sigma, rho: int, threads: int | None = None, spatial: str = "box"):
+    """eq.(1)-(3) P:54-67, fp64 -> g (float64).  ``spatial``: "box" (omega = 1 on
+    the (2 rho + 1)^2 box, reading R1) or "gauss" (eq.(4): exp(-|j|^2 / 2 rho^2)
+    on [-3 rho, 3 rho]^2)."""
     lib = _load()
+    fn = {"box": lib.fabfo_brute, "gauss": lib.fabfo_brute_gauss}[spatial]
     f, th, sg = _as3d(img), _as3d(theta), _as3d(sigma)
     B, H, W = f.shape
     g = np.empty(f.shape, np.float64)
 
     def run(p0, p1):
-        if lib.fabfo_brute(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, p0, p1, _ptr(g)):
+        if fn(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, p0, p1, _ptr(g)):
             raise ValueError("fabfo_brute: invalid arguments")
 
     _parallel(f.size, run, threads, chunk=2048)
     return g.reshape(np.shape(img))
 
 
-def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None = None):
+def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None = None, spatial: str = "box"):
     """Algorithm 1 / eq.(29) in __float128.
 
     Returns a dict of arrays: ``g_lit`` (eq.(29) as printed), ``g_guard`` (with the
@@ -135,6 +141,7 @@ def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None =
     list; otherwise they have the image's shape.
     """
     lib = _load()
+    fn = {"box": lib.fabfo_fast, "gauss": lib.fabfo_fast_gauss}[spatial]
     f, th, sg = _as3d(img), _as3d(theta), _as3d(sigma)
     B, H, W = f.shape
     if pixels is not None:
@@ -152,13 +159,13 @@ def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None =
     }
 
     def run(p0, p1):
-        rc = lib.fabfo_fast(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, N, _ptr(idx), p0, p1,
+        rc = fn(_ptr(f), _ptr(th), _ptr(sg), B, H, W, rho, N, _ptr(idx), p0, p1,
                             _ptr(out["g_lit"]), _ptr(out["g_guard"]), _ptr(out["kappa"]),
                             _ptr(out["t2n"]), _ptr(out["code"]))
         if rc:
             raise ValueError("fabfo_fast: invalid arguments")
 
-    n = (2 * rho + 1) ** 2
+    n = (2 * (3 * rho if spatial == "gauss" else rho) + 1) ** 2
     _parallel(total, run, threads, chunk=max(16, min(4096, 400000 // max(1, n * (N + 1)))))
     if pixels is None:
         shp = np.shape(img)
@@ -166,7 +173,7 @@ def fast(img, theta, sigma, rho: int, N: int, pixels=None, threads: int | None =
     return out
 
 
-def fast_window(vals, f_center: float, theta: float, sigma: float, N: int, route: int = 0):
+def fast_window(vals, f_center: float, theta: float, sigma: float, N: int, route: int = 0, weights=None):
     """g-hat for one explicit window (samples ``vals``): dict of scalars.
 
     ``route`` selects how eq.(22) is summed: 0 over the window's distinct values
@@ -176,6 +183,12 @@ def fast_window(vals, f_center: float, theta: float, sigma: float, N: int, route
     v = _f32(vals).ravel()
     o = np.empty(6, np.float64)
     code = ctypes.c_int(0)
+    if weights is not None:  # omega(j) = weights[j] (the weighted histogram of eq.(5))
+        wt = np.ascontiguousarray(weights, np.float64).ravel()
+        if wt.size != v.size or lib.fabfo_window_w(_ptr(v), _ptr(wt), v.size, float(f_center), float(theta),
+                                                   float(sigma), N, int(route), _ptr(o), ctypes.byref(code)):
+            raise ValueError("fabfo_window_w: invalid arguments")
+        return dict(g_lit=o[0], g_guard=o[1], kappa=o[2], t2n=o[3], lam=o[4], t0=o[5], code=code.value)
     if lib.fabfo_window(_ptr(v), v.size, float(f_center), float(theta), float(sigma), N, int(route), _ptr(o),
                         ctypes.byref(code)):
         raise ValueError("fabfo_window: invalid arguments")

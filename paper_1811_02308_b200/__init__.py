@@ -16,6 +16,9 @@ from .fabf import (  # noqa: F401
     filter_host,
     filter_interleaved,
     filter_mozerov,
+    filter_sharpen,
+    sharpen_maps,
+    SHARPEN_DEFAULTS,
     filter_profile,
     lib,
     library_path,

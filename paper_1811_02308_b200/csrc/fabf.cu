@@ -1371,6 +1371,81 @@ __global__ void __launch_bounds__(kThreads) k_mozerov(const float* __restrict__ 
 }
 
 // ============================================================================
+// NEXT-2: the sharpening application's range-kernel maps, produced
+// on the device from f alone so that only f crosses PCIe:
+//   theta = f + (f - fbar), fbar = the box mean over Omega (half-width rho);
+//   sigma = s_hi - (s_hi - s_lo) min(|LoG f| / l_sat, 1)         (reading R15)
+// with LoG the sampled normalised Gaussian of scale s (|x| <= ceil(4 s)) and its
+// analytic second derivative, separable: L = g''_x g_y + g_x g''_y.  One CTA per
+// T x T tile: footprint staged in shared memory (reflected borders), box sums
+// by sliding windows in fp64, the two LoG terms by separable fp32 passes.
+constexpr int kMaxLogR = 16;
+__constant__ float c_log_g[2 * kMaxLogR + 1], c_log_g2[2 * kMaxLogR + 1];
+
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_sharpen_maps(const float* __restrict__ img,
+                                                            float* __restrict__ theta, float* __restrict__ sigma,
+                                                            int H, int W, int rho, int rl, float s_lo, float s_hi,
+                                                            float inv_sat) {
+  extern __shared__ __align__(16) unsigned char sms[];
+  const int R = max(rho, rl), FS = T + 2 * R, w = 2 * rho + 1;
+  double* Hs = reinterpret_cast<double*>(sms);                            // [T + 2 rho][T] box row sums
+  float* F = reinterpret_cast<float*>(sms + sizeof(double) * (T + 2 * rho) * T);  // [FS][FS]
+  float* Ga = F + FS * FS;                                                 // [T + 2 rl][T]: g_x * f
+  float* Gb = Ga + (T + 2 * rl) * T;                                       // [T + 2 rl][T]: g''_x * f
+  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T, b = blockIdx.z;
+  const size_t plane = (size_t)b * H * W;
+  const float* src = img + plane;
+  for (int t = threadIdx.x; t < FS * FS; t += kThreads) {
+    const int r = t / FS, cc = t - r * FS;
+    F[t] = __ldg(src + (size_t)reflect_index(y0 - R + r, H) * W + reflect_index(x0 - R + cc, W));
+  }
+  __syncthreads();
+  // box: rows R - rho .. R + rho + T - 1 of the footprint, sliding sums
+  for (int r = threadIdx.x; r < T + 2 * rho; r += kThreads) {
+    const float* Fr = F + (r + R - rho) * FS + (R - rho);
+    double acc = 0.0;
+    for (int cc = 0; cc < w; ++cc) acc += Fr[cc];
+    Hs[r * T] = acc;
+    for (int x = 1; x < T; ++x) {
+      acc += (double)Fr[x + w - 1] - (double)Fr[x - 1];
+      Hs[r * T + x] = acc;
+    }
+  }
+  // LoG, horizontal pass: rows R - rl .. R + rl + T - 1
+  for (int t = threadIdx.x; t < (T + 2 * rl) * T; t += kThreads) {
+    const int r = t / T, x = t - r * T;
+    const float* Fr = F + (r + R - rl) * FS + (R - rl) + x;
+    float a = 0.f, bb = 0.f;
+    for (int k = 0; k <= 2 * rl; ++k) {  // tap k <-> offset dx = rl - k (convolution)
+      const float v = Fr[2 * rl - k];
+      a = fmaf(c_log_g[k], v, a);
+      bb = fmaf(c_log_g2[k], v, bb);
+    }
+    Ga[t] = a;
+    Gb[t] = bb;
+  }
+  __syncthreads();
+  const float inv_n = 1.0f / (float)(w * w);
+  for (int t = threadIdx.x; t < T * T; t += kThreads) {
+    const int y = t / T, x = t - y * T;
+    const int yy = y0 + y, xx = x0 + x;
+    if (yy >= H || xx >= W) continue;
+    double acc = 0.0;
+    for (int dy = 0; dy < w; ++dy) acc += Hs[(y + dy) * T + x];
+    float L = 0.f;
+    for (int k = 0; k <= 2 * rl; ++k) {
+      const int rr = (y + 2 * rl - k) * T + x;
+      L = fmaf(c_log_g2[k], Ga[rr], fmaf(c_log_g[k], Gb[rr], L));
+    }
+    const double f = (double)F[(y + R) * FS + x + R];
+    const size_t o = plane + (size_t)yy * W + xx;
+    theta[o] = (float)(2.0 * f - acc * (double)inv_n);
+    sigma[o] = s_hi - (s_hi - s_lo) * fminf(fabsf(L) * inv_sat, 1.0f);
+  }
+}
+
+// ============================================================================
 // colour (NEXT-3): channel-interleaved images (B x H x W x C) <-> the planar
 // batch (B C) x H x W the filter runs on, channel by channel as the paper
 // filters colour images.  Pure data movement, coalesced on the
@@ -2044,6 +2119,82 @@ fabf_status_t fabf_filter_mozerov(fabf_plan_t plan, const float* img, const floa
   FABF_CUDA(cudaGetLastError(), "k_mozerov launch");
   p->launches = 1;
   p->last_stream = st;
+  return FABF_OK;
+}
+
+fabf_status_t fabf_sharpen_maps(fabf_plan_t plan, const float* img, int rho, const fabf_sharpen_t* prm,
+                                float* theta, float* sigma, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  fabf_status_t s = validate_common(p, rho);
+  if (s != FABF_OK) return s;
+  if (!img || !theta || !sigma || !prm) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!(prm->log_scale > 0.0f) || !(prm->log_sat > 0.0f) || !(prm->sigma_lo > 0.0f) ||
+      !(prm->sigma_hi >= prm->sigma_lo))
+    return fail(FABF_ERR_INVALID_ARGUMENT, "sharpen parameters: log_scale, log_sat, sigma_lo > 0, sigma_hi >= sigma_lo");
+  const int rl = (int)ceilf(4.0f * prm->log_scale);
+  if (rl > kMaxLogR || 2 * rl + 1 > p->H || 2 * rl + 1 > p->W)
+    return fail(FABF_ERR_INVALID_ARGUMENT, "log_scale too large (ceil(4 s) <= 16 and its window inside the image)");
+  const size_t bytes = sizeof(float) * (size_t)p->B * p->H * p->W;
+  if (overlaps(theta, bytes, img, bytes) || overlaps(sigma, bytes, img, bytes) || overlaps(theta, bytes, sigma, bytes))
+    return fail(FABF_ERR_INVALID_ARGUMENT, "outputs overlap");
+  constexpr int T = 32;
+  const int R = std::max(rho, rl), FS = T + 2 * R;
+  const size_t smem = sizeof(double) * (T + 2 * rho) * T + sizeof(float) * ((size_t)FS * FS + 2 * (T + 2 * rl) * T);
+  if (smem > (size_t)kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for the map producer");
+  cudaStream_t st = (cudaStream_t)stream;
+  {  // taps (host, double -> float), per call on the stream
+    float hg[2 * kMaxLogR + 1] = {}, hg2[2 * kMaxLogR + 1] = {};
+    double g[2 * kMaxLogR + 1], gs = 0.0, sc = prm->log_scale;
+    for (int k = -rl; k <= rl; ++k) gs += (g[k + rl] = std::exp(-0.5 * k * k / (sc * sc)));
+    for (int k = -rl; k <= rl; ++k) {
+      hg[k + rl] = (float)(g[k + rl] / gs);
+      hg2[k + rl] = (float)(((double)k * k - sc * sc) / (sc * sc * sc * sc) * g[k + rl] / gs);
+    }
+    FABF_CUDA(cudaMemcpyToSymbolAsync(c_log_g, hg, sizeof(hg), 0, cudaMemcpyHostToDevice, st), "taps");
+    FABF_CUDA(cudaMemcpyToSymbolAsync(c_log_g2, hg2, sizeof(hg2), 0, cudaMemcpyHostToDevice, st), "taps");
+  }
+  {
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[p->device]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_sharpen_maps<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_sharpen_maps)");
+      attr_set[p->device] = true;
+    }
+  }
+  dim3 g((p->W + T - 1) / T, (p->H + T - 1) / T, p->B);
+  k_sharpen_maps<T><<<g, kThreads, smem, st>>>(img, theta, sigma, p->H, p->W, rho, rl, prm->sigma_lo,
+                                               prm->sigma_hi, 1.0f / prm->log_sat);
+  FABF_CUDA(cudaGetLastError(), "k_sharpen_maps launch");
+  ++g_launches;
+  return FABF_OK;
+}
+
+fabf_status_t fabf_filter_sharpen(fabf_plan_t plan, const float* img, int rho, int N, const fabf_sharpen_t* prm,
+                                  float* out, void* stream) {
+  // the application pipeline: maps from f (plan-owned planes), then Algorithm 1
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  if (!p) return fail(FABF_ERR_INVALID_ARGUMENT, "plan is NULL");
+  {
+    fabf_status_t s0 = check_plan_device(p);
+    if (s0 != FABF_OK) return s0;
+  }
+  const size_t px = (size_t)p->B * p->H * p->W;
+  if (!p->h_in) {  // planar staging (shared with fabf_filter_host), allocated on first use
+    cudaError_t e;
+    if ((e = cudaMalloc(&p->h_in, 3 * sizeof(float) * staging_pitch(px))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(staging)");
+    if ((e = cudaMalloc(&p->h_out, px * sizeof(float))) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+  }
+  float* th = p->h_in + staging_pitch(px);
+  float* sg = p->h_in + 2 * staging_pitch(px);
+  g_launches = 0;
+  fabf_status_t s = fabf_sharpen_maps(plan, img, rho, prm, th, sg, stream);
+  if (s != FABF_OK) return s;
+  const int maps = g_launches;
+  s = filter_impl(p, img, th, sg, rho, N, out, nullptr, (cudaStream_t)stream);
+  if (s != FABF_OK) return s;
+  p->launches += maps;
   return FABF_OK;
 }
 

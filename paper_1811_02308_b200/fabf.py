@@ -35,6 +35,14 @@ class FabfError(RuntimeError):
         self.status = status
 
 
+class _Sharpen(ctypes.Structure):
+    _fields_ = [("log_scale", ctypes.c_float), ("sigma_lo", ctypes.c_float), ("sigma_hi", ctypes.c_float),
+                ("log_sat", ctypes.c_float)]
+
+
+SHARPEN_DEFAULTS = dict(log_scale=1.0, sigma_lo=10.0, sigma_hi=40.0, log_sat=20.0)
+
+
 class _Diag(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_void_p), ("beta", ctypes.c_void_p), ("kappa", ctypes.c_void_p),
                 ("t2n", ctypes.c_void_p), ("code", ctypes.c_void_p)]
@@ -61,6 +69,11 @@ def lib():
             L.fabf_filter_profile.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_float)]
             L.fabf_filter_events.argtypes = [P, P, P, P, i, i, P, P, ctypes.POINTER(ctypes.c_void_p)]
             L.fabf_last_fallback_count.argtypes = [P, ctypes.POINTER(ctypes.c_longlong)]
+            if hasattr(L, "fabf_filter_sharpen"):
+                L.fabf_sharpen_maps.argtypes = [P, P, i, ctypes.POINTER(_Sharpen), P, P, P]
+                L.fabf_sharpen_maps.restype = ctypes.c_int
+                L.fabf_filter_sharpen.argtypes = [P, P, i, i, ctypes.POINTER(_Sharpen), P, P]
+                L.fabf_filter_sharpen.restype = ctypes.c_int
             if hasattr(L, "fabf_filter_mozerov"):
                 L.fabf_filter_mozerov.argtypes = [P, P, P, P, i, P, P]
                 L.fabf_filter_mozerov.restype = ctypes.c_int
@@ -301,4 +314,34 @@ def filter_mozerov(plan: Plan, img, theta, sigma, rho: int, out=None, stream=Non
     _check(lib().fabf_filter_mozerov(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
                                      _dev_ptr(sigma, "sigma", plan), int(rho), _dev_ptr(out, "out", plan),
                                      _stream_ptr(stream)))
+    return out
+
+
+def _sharpen_params(kw):
+    prm = dict(SHARPEN_DEFAULTS)
+    prm.update(kw)
+    return _Sharpen(*(float(prm[k]) for k in ("log_scale", "sigma_lo", "sigma_hi", "log_sat")))
+
+
+def sharpen_maps(plan: Plan, img, rho: int, theta=None, sigma=None, stream=None, **params):
+    """fabf_sharpen_maps: (theta, sigma) of the sharpening application."""
+    import torch
+
+    theta = torch.empty_like(img) if theta is None else theta
+    sigma = torch.empty_like(img) if sigma is None else sigma
+    prm = _sharpen_params(params)
+    _check(lib().fabf_sharpen_maps(plan.handle, _dev_ptr(img, "img", plan), int(rho), ctypes.byref(prm),
+                                   _dev_ptr(theta, "theta", plan), _dev_ptr(sigma, "sigma", plan),
+                                   _stream_ptr(stream)))
+    return theta, sigma
+
+
+def filter_sharpen(plan: Plan, img, rho: int, N: int, out=None, stream=None, **params):
+    """fabf_filter_sharpen: the sharpening application end to end on device tensors."""
+    import torch
+
+    out = torch.empty_like(img) if out is None else out
+    prm = _sharpen_params(params)
+    _check(lib().fabf_filter_sharpen(plan.handle, _dev_ptr(img, "img", plan), int(rho), int(N), ctypes.byref(prm),
+                                     _dev_ptr(out, "out", plan), _stream_ptr(stream)))
     return out

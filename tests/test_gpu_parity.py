@@ -523,3 +523,35 @@ def test_mozerov_baseline(fb, orc, kind, shape, rho):
     sc = grey_scale(w.img)
     err = np.abs(out.cpu().numpy().astype(np.float64) - ref) / sc
     assert err.max() <= TOL_GREY, f"max |delta| = {err.max()} grey"
+
+
+@pytest.mark.parametrize("kind,shape,rho,N,prm", [
+    ("voronoi", (1, 160, 200), 5, 5, {}),
+    ("texture", (2, 97, 131), 3, 6, dict(log_scale=0.8, sigma_lo=6.0, sigma_hi=30.0, log_sat=10.0)),
+    ("rect", (1, 120, 90), 12, 8, dict(log_scale=2.0, sigma_lo=12.0, sigma_hi=45.0, log_sat=25.0))])
+def test_sharpen_application(fb, orc, kind, shape, rho, N, prm):
+    """NEXT-2: the device maps equal the oracle's (theta to fp32
+    rounding of the box mean, sigma to fp32 LoG rounding), and the whole
+    application (maps + Algorithm 1 from f alone) matches the oracle run on
+    those maps, every pixel."""
+    import torch
+
+    w = workloads.random_case(*shape, seed=71, kind=kind, rho=rho, N=N)
+    plan = fb.Plan(*w.shape)
+    full = dict(fb.SHARPEN_DEFAULTS)
+    full.update(prm)
+    th, sg = fb.sharpen_maps(plan, _dev(w.img), rho, **prm)
+    out = fb.filter_sharpen(plan, _dev(w.img), rho, N, **prm)
+    torch.cuda.synchronize()
+    th, sg, out = th.cpu().numpy(), sg.cpu().numpy(), out.cpu().numpy()
+    rth, rsg = orc.sharpen_maps(w.img, rho, **full)
+    assert np.max(np.abs(th - rth)) < 1e-3
+    assert np.max(np.abs(sg - rsg)) < 1e-3
+    assert sg.min() >= full["sigma_lo"] - 1e-4 and sg.max() <= full["sigma_hi"] + 1e-4
+    o = orc.fast(w.img, th, sg, rho, N)
+    mx, nbad, _ = compare_guarded(out, o, 1.0)
+    assert nbad == 0, f"max |delta| = {mx} grey"
+    o2 = orc.fast(w.img, rth.astype(np.float32), rsg.astype(np.float32), rho, N)
+    mx2, nbad2, _ = compare_guarded(out, o2, 1.0)
+    assert nbad2 == 0, f"against the oracle's own maps: max |delta| = {mx2} grey"
+    assert plan.last_launch_count() >= 2

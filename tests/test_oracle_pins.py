@@ -470,3 +470,83 @@ def test_sharpen_maps_against_scipy(orc, rho, s):
     ref = 35.0 - (35.0 - 8.0) * np.minimum(np.abs(L) / 12.0, 1.0)
     assert np.max(np.abs(sg[0] - ref)) < 1e-9
     assert sg.min() >= 8.0 and sg.max() <= 35.0
+
+
+# ---------------------------------------------------------------- NEXT-1: Gaussian omega, eq.(4)
+def _gauss_w(rho):
+    R = 3 * rho
+    d = np.arange(-R, R + 1)
+    return np.exp(-(d[:, None] ** 2 + d[None, :] ** 2) / (2.0 * rho * rho))
+
+
+def _ghat_projection_mp_w(vals, wts, theta, sigma, N):
+    """eq.(29) with the weighted histogram of eq.(5): the projection identity
+    with weights, sum_k c_k I_k = sum_j w_j (Pi_N psi)(t_j); mpmath, no Hilbert
+    matrix, no recursion."""
+    a, b = mp.mpf(float(min(vals))), mp.mpf(float(max(vals)))
+    d = b - a
+    lam = d ** 2 / (2 * mp.mpf(float(sigma)) ** 2)
+    t0 = (mp.mpf(float(theta)) - a) / d
+    psi = lambda t: mp.e ** (-lam * (t - t0) ** 2)
+    P = lambda k, t: mp.legendre(k, 2 * t - 1)
+    pts = sorted({mp.mpf(0), min(max(t0, mp.mpf(0)), mp.mpf(1)), mp.mpf(1)})
+    J = [mp.quad(lambda t: P(k, t) * psi(t), pts) for k in range(N + 1)]
+    Jt = [mp.quad(lambda t: t * P(k, t) * psi(t), pts) for k in range(N + 1)]
+    ts = [(mp.mpf(float(v)) - a) / d for v in vals]
+    ws = [mp.mpf(float(x)) for x in wts]
+    num = den = mp.mpf(0)
+    for k in range(N + 1):
+        nu = mp.fsum(wj * P(k, t) for wj, t in zip(ws, ts))
+        den += (2 * k + 1) * nu * J[k]
+        num += (2 * k + 1) * nu * Jt[k]
+    return float(a + d * num / den)
+
+
+@pytest.mark.parametrize("N", [0, 2, 5, 8])
+def test_gauss_window_projection_identity_and_routes(orc, N):
+    rng = np.random.default_rng(500 + N)
+    wts = _gauss_w(2).ravel()  # 13 x 13
+    for trial in range(2):
+        vals = np.rint(rng.normal(110, 35, wts.size)).clip(0, 255).astype(np.float32)
+        if trial:
+            vals[::3] = rng.integers(200, 255, vals[::3].size)
+        theta = float(np.float32(vals[wts.size // 2] + rng.uniform(-10, 10)))
+        sigma = float(np.float32(rng.uniform(10, 50)))
+        o = orc.fast_window(vals, vals[wts.size // 2], theta, sigma, N, weights=wts)
+        o1 = orc.fast_window(vals, vals[wts.size // 2], theta, sigma, N, route=1, weights=wts)
+        ref = _ghat_projection_mp_w(vals, wts, theta, sigma, N)
+        span = float(vals.max() - vals.min())
+        assert abs(o["g_lit"] - ref) <= 1e-9 * span, (trial, o["g_lit"], ref)
+        assert o["g_lit"] == pytest.approx(o1["g_lit"], rel=1e-13, abs=1e-13)
+        # the weighted and the unweighted filters differ (the weights matter)
+        if N >= 2:
+            ob = orc.fast_window(vals, vals[wts.size // 2], theta, sigma, N)
+            assert abs(ob["g_lit"] - o["g_lit"]) > 1e-6
+
+
+def test_gauss_image_routes_limits_and_brute(orc):
+    """fast(spatial="gauss") equals the weighted window route pixel by pixel;
+    sigma -> inf gives the Gaussian-weighted mean (N >= 1); brute force with the
+    Gaussian omega equals an independent numpy implementation."""
+    rho = 2
+    w = workloads.random_case(1, 19, 23, seed=9, kind="rect", rho=rho, N=4)
+    R = 3 * rho
+    W2 = _gauss_w(rho)
+    pad = np.pad(w.img[0].astype(np.float64), R, mode="symmetric")
+    o = orc.fast(w.img, w.theta, w.sigma, rho, 4, spatial="gauss")
+    for (y, x) in [(0, 0), (9, 11), (18, 22), (4, 20)]:
+        win = pad[y:y + 2 * R + 1, x:x + 2 * R + 1].astype(np.float32)
+        r = orc.fast_window(win, w.img[0, y, x], w.theta[0, y, x], w.sigma[0, y, x], 4, weights=W2)
+        assert o["g_lit"][0, y, x] == r["g_lit"] and o["g_guard"][0, y, x] == r["g_guard"]
+    big = orc.fast(w.img, w.theta, np.full_like(w.sigma, 1e7), rho, 3, spatial="gauss")
+    mean = np.array([[np.sum(W2 * pad[y:y + 2 * R + 1, x:x + 2 * R + 1]) / W2.sum() for x in range(23)]
+                     for y in range(19)])
+    assert np.max(np.abs(big["g_guard"][0] - mean)) < 1e-6
+    g = orc.brute(w.img, w.theta, w.sigma, rho, spatial="gauss")
+    ref = np.empty((19, 23))
+    for y in range(19):
+        for x in range(23):
+            v = pad[y:y + 2 * R + 1, x:x + 2 * R + 1]
+            k = W2 * np.exp(-(v - w.theta[0, y, x]) ** 2 / (2.0 * float(w.sigma[0, y, x]) ** 2))
+            ref[y, x] = np.sum(k * v) / np.sum(k)
+    assert np.max(np.abs(g[0] - ref)) < 1e-9
