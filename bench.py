@@ -313,6 +313,7 @@ def run_gpu(args):
     fused = {} if args.no_other_configs else fused_variant(fb, w, img, th, sg, flush)
     colour = {} if args.no_other_configs else colour_variant(fb, dev, flush)
     sharpen = {} if args.no_other_configs else sharpen_variant(fb, dev, flush)
+    gauss = {} if args.no_other_configs else gauss_variant(fb, dev, flush)
     others = {} if args.no_other_configs else other_configs(fb, dev, flush)
 
     # end to end through the C ABI with host buffers (pinned), copies inside
@@ -383,6 +384,7 @@ def run_gpu(args):
             "fused_variant": fused,
             "colour_variant": colour,
             "sharpen_variant": sharpen,
+            "gauss_variant": gauss,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
@@ -533,6 +535,41 @@ def sharpen_variant(fb, dev, flush, steps: int = 10):
                      "e2e Mpix/s": H * W / e2e_s / 1e6, "e2e_ms": e2e_s * 1e3,
                      "h2d_bytes_per_frame": 4 * H * W, "d2h_bytes_per_frame": 4 * H * W,
                      "params": dict(fb.SHARPEN_DEFAULTS)}
+    return res
+
+
+def gauss_variant(fb, dev, flush, steps: int = 10):
+    """NEXT-1: Algorithm 1 with the paper's Gaussian omega (eq.(4) on [-3 rho,
+    3 rho]^2, fabf_filter_gauss): the classical filter of Table II (theta = f,
+    sigma = 40) on 512x512 at rho = 3 / 5 / 10, N = 5 (the paper: 171-189 ms
+    each on MATLAB / 3.4 GHz), and a 4K frame at rho = 5, N = 5.
+    Synthetic Voronoi + noise images.  Device-timed."""
+    import torch
+
+    import workloads
+
+    res = {}
+    cases = [(512, 512, r, 5) for r in (3, 5, 10)] + [(2160, 3840, 5, 5)]
+    for (H, W, rho, N) in cases:
+        f = workloads.voronoi(H, W, seed=9000 + H, n_seeds=96, noise_sd=12.0).astype(np.float32)[None]
+        img = torch.from_numpy(f).to(dev)
+        sg = torch.full_like(img, 40.0)
+        out = torch.empty_like(img)
+        plan = fb.Plan(1, H, W)
+        stream = torch.cuda.current_stream()
+        for _ in range(3):
+            fb.filter_gauss(plan, img, img, sg, rho, N, out=out)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in ev:
+            flush.fill_(1.0)
+            a.record(stream)
+            fb.filter_gauss(plan, img, img, sg, rho, N, out=out)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        res[f"gauss_{W}x{H}_rho{rho}_N{N}"] = {"Mpix/s": H * W / (ms * 1e-3) / 1e6, "ms": ms,
+                                               "launches": plan.last_launch_count(),
+                                               "fallback_pixels": plan.last_fallback_count()}
     return res
 
 

@@ -128,6 +128,18 @@ fabf_status_t fabf_bounds(fabf_plan_t plan, const float* img, int rho, float* al
 fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* theta,
                                const float* sigma, int rho, int N, float* out, void* stream);
 
+/* NEXT-1: the paper's default spatial kernel (eq.(4)): omega(j) =
+ * exp(-|j|^2 / 2 rho^2) on Omega = [-3 rho, 3 rho]^2 instead of the box.  The
+ * bounds alpha, beta are the min / max over that whole window (every sample has
+ * omega > 0); the moments of Algorithm 1 line 6 are Gaussian-weighted, by
+ * exact separable FIR in fp64 (O(rho) per pixel and power -- the paper's own
+ * runs used direct FIR too).  Same pointer rules, flags and errors as
+ * fabf_filter with the window half-width 3 rho: 6 rho + 1 <= min(height,
+ * width), 0 <= rho <= 16.  Three kernels (bounds, moments + per-pixel, exact
+ * fallback).                                                                 */
+fabf_status_t fabf_filter_gauss(fabf_plan_t plan, const float* img, const float* theta, const float* sigma,
+                                int rho, int N, float* out, void* stream);
+
 /* NEXT-2: the sharpening / noise-removal application (after Zhang &
  * Allebach): the range-kernel maps are produced on the device from f alone,
  *   theta(i) = f(i) + zeta(i), zeta = f - fbar (fbar: box mean over the same

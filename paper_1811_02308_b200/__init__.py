@@ -16,6 +16,7 @@ from .fabf import (  # noqa: F401
     filter_host,
     filter_interleaved,
     filter_mozerov,
+    filter_gauss,
     filter_sharpen,
     sharpen_maps,
     SHARPEN_DEFAULTS,

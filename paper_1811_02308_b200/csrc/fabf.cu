@@ -1310,6 +1310,157 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
 }
 
 // ============================================================================
+// NEXT-1: the paper's default spatial kernel, eq.(4): omega(j) =
+// exp(-|j|^2 / 2 rho^2) on Omega = [-3 rho, 3 rho]^2.  The moments gamma_k =
+// omega * f^k of Algorithm 1 line 6 are separable Gaussian convolutions
+// (the paper used direct FIR, "imfilter"); here exact sampled
+// FIR in fp64, separable, O(rho) per pixel and power.  One CTA per T x T tile:
+//   stage the (T + 2R)^2 footprint (R = 3 rho, reflected borders); its min/max
+//   give the tile-local centre c_T and power-of-two scale s_T (u exact);
+//   for q = 1..N: P <- P u over the footprint, vertical FIR of P into V,
+//   horizontal FIR of V into S_q (all fp64, shared memory);
+//   per pixel: alpha, beta from k_bounds (half-width R: every j in Omega has
+//   omega(j) > 0, so Lambda_i is the whole box), the stretch / fit / integrals /
+//   ratio of fabf_device.cuh with nu_0 = sum omega; pixels whose centring
+//   amplification is too large go to k_fallback_gauss (exact weighted sums).
+__constant__ double c_gw[2 * 48 + 1];  // omega's 1-D factor exp(-d^2 / 2 rho^2), d = -R..R
+
+template <int T>
+__host__ __device__ constexpr size_t gauss_smem(int R, int N) {
+  return sizeof(double) * ((size_t)(T + 2 * R) * (T + 2 * R) + (size_t)T * (T + 2 * R) + (size_t)(N > 0 ? N : 1) * T * T) +
+         sizeof(float) * (size_t)(T + 2 * R) * (T + 2 * R);
+}
+
+template <int N, int T>
+__global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, float nu0f) {
+  extern __shared__ __align__(16) unsigned char smg[];
+  constexpr int NN = N > 0 ? N : 1;
+  const int FS = T + 2 * R, H = a.H, W = a.W;
+  double* P = reinterpret_cast<double*>(smg);  // [FS][FS] current power of u
+  double* V = P + FS * FS;                     // [T][FS] vertical FIR of P
+  double* S = V + T * FS;                      // [NN][T][T] moments
+  float* F = reinterpret_cast<float*>(S + NN * T * T);  // [FS][FS]
+  __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T, b = blockIdx.z;
+  const size_t plane = (size_t)(a.b0 + b) * H * W;
+  const float* src = a.img + plane;
+  float lmin = CUDART_INF_F, lmax = -CUDART_INF_F;
+  for (int t = tid; t < FS * FS; t += kThreads) {
+    const int r = t / FS, cc = t - r * FS;
+    const float v = __ldg(src + (size_t)reflect_index(y0 - R + r, H) * W + reflect_index(x0 - R + cc, W));
+    F[t] = v;
+    lmin = fminf(lmin, v);
+    lmax = fmaxf(lmax, v);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
+    lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
+  }
+  if (lane == 0) red_min[warp] = lmin, red_max[warp] = lmax;
+  __syncthreads();
+  lmin = red_min[0], lmax = red_max[0];
+  for (int i = 1; i < kThreads / 32; ++i) lmin = fminf(lmin, red_min[i]), lmax = fmaxf(lmax, red_max[i]);
+  const double cT = 0.5 * ((double)lmin + (double)lmax), halfr = 0.5 * ((double)lmax - (double)lmin);
+  int e2 = 0;
+  if (halfr > 0.0) frexp(halfr, &e2);
+  const double invS = ldexp(1.0, -e2), mcs = -cT * invS;  // u = f invS + mcs, exact
+  for (int t = tid; t < FS * FS; t += kThreads) P[t] = 1.0;
+  for (int q = 0; q < N; ++q) {
+    __syncthreads();
+    for (int t = tid; t < FS * FS; t += kThreads) P[t] *= fma((double)F[t], invS, mcs);
+    __syncthreads();
+    for (int t = tid; t < T * FS; t += kThreads) {  // vertical: rows r .. r + 2R of column cc
+      const int r = t / FS, cc = t - r * FS;
+      const double* col = P + r * FS + cc;
+      double acc = 0.0;
+      for (int d = 0; d <= 2 * R; ++d) acc = fma(c_gw[d], col[d * FS], acc);
+      V[t] = acc;
+    }
+    __syncthreads();
+    for (int t = tid; t < T * T; t += kThreads) {  // horizontal: columns x .. x + 2R of row r
+      const int r = t / T, x = t - r * T;
+      const double* row = V + r * FS + x;
+      double acc = 0.0;
+      for (int d = 0; d <= 2 * R; ++d) acc = fma(c_gw[d], row[d], acc);
+      S[q * T * T + t] = acc;
+    }
+  }
+  __syncthreads();
+  const float n = nu0f;
+  for (int t = tid; t < T * T; t += kThreads) {
+    const int r = t / T, x = t - r * T, yy = y0 + r, xx = x0 + x;
+    if (yy >= H || xx >= W) continue;
+    const int o = (int)plane + yy * W + xx;
+    const float al = __ldg(a.alpha + o), be = __ldg(a.beta + o);
+    if (al == be) {  // P:204, Algorithm 1 lines 4-5
+      a.out[o] = al;
+      continue;
+    }
+    const double au = fma((double)al, invS, mcs), bu = fma((double)be, invS, mcs);
+    if (stretch_flagged(au, bu, a.flag_root)) {
+      const int slot = atomicAdd(a.fb_count, 1);
+      a.fb_list[slot] = o;
+      continue;
+    }
+    double Sq[N + 1], nup[NN];
+    Sq[0] = (double)n;
+#pragma unroll
+    for (int q = 1; q <= N; ++q) Sq[q] = S[(q - 1) * T * T + t];
+    nu_from_sums<N>(Sq, au, bu, nup, 1);
+    const float th = __ldg(a.theta + o), sg = __ldg(a.sigma + o);
+    float lam, t0;
+    const int regime = range_params(al, be, th, sg, lam, t0);
+    const PixelResult res = ghat_from_record<N>(nup, 1, th, sg, al, be, regime, a.flags, false, n);
+    a.out[o] = res.g;
+  }
+}
+
+// exact weighted moments for the flagged pixels of k_gauss (thread per pixel):
+// nu_k = sum_j omega(j) P_k(w_j) with the pixel's own stretch (cf. k_fallback)
+template <int N>
+__global__ void __launch_bounds__(kThreads) k_fallback_gauss(FilterArgs a, int R, float nu0f) {
+  const int count = *a.fb_count;
+  const int H = a.H, W = a.W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const int o = a.fb_list[i];
+    const int b = o / (H * W), rem = o - b * H * W, y = rem / W, x = rem - y * W;
+    const float* img = a.img + (size_t)b * H * W;
+    const float al = a.alpha[o], be = a.beta[o];
+    const double mid = 0.5 * ((double)al + (double)be), ih = 2.0 / ((double)be - (double)al);
+    double acc[N + 1];
+#pragma unroll
+    for (int k = 0; k <= N; ++k) acc[k] = 0.0;
+    for (int dy = -R; dy <= R; ++dy) {
+      const float* row = img + reflect_index(y + dy, H) * W;
+      const double wy = c_gw[dy + R];
+      for (int dx = -R; dx <= R; ++dx) {
+        const double wgt = wy * c_gw[dx + R];
+        const double sv = ((double)__ldg(row + reflect_index(x + dx, W)) - mid) * ih;
+        double r0 = 1.0, r1 = sv;
+        acc[0] += wgt;
+        if (N >= 1) acc[1] += wgt * sv;
+#pragma unroll
+        for (int k = 1; k < N; ++k) {
+          const double r2 = fma(-(double)(k * k) / (double)(4 * k * k - 1), r0, sv * r1);
+          acc[k + 1] = fma(wgt, r2, acc[k + 1]);
+          r0 = r1;
+          r1 = r2;
+        }
+      }
+    }
+    double nu[N + 1];
+#pragma unroll
+    for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * c_monic_scale[k] * acc[k];
+    float lam, t0;
+    const float th = a.theta[o], sg = a.sigma[o];
+    const int regime = range_params(al, be, th, sg, lam, t0);
+    const PixelResult res = ghat_from_record<N>(nu + 1, 1, th, sg, al, be, regime, a.flags, false, nu0f);
+    a.out[o] = res.g;
+  }
+}
+
+// ============================================================================
 // Mozerov & van de Weijer's uniform-prior filter (NEXT-4), the baseline the
 // paper compares with (Fig.3): a degree-0 fit of the local
 // histogram on [f(i), 2 fbar(i) - f(i)] (Delta = 0) instead of [alpha, beta],
@@ -1890,6 +2041,44 @@ cudaError_t alloc_ring(Plan* p) {
 // planes of px floats, each starting 16-byte aligned
 size_t staging_pitch(size_t px) { return (px + 3) & ~(size_t)3; }
 
+// NEXT-1 launches: k_gauss on T x T tiles (T = 32 for rho <= 10, else 16 so
+// that the fp64 footprint fits), then the exact weighted fallback
+constexpr int kMaxGaussRho = 16;
+template <int N>
+fabf_status_t launch_gauss(FilterArgs& fa, int R, float nu0, cudaStream_t st) {
+  const bool big = R <= 30;
+  const size_t smem = big ? gauss_smem<32>(R, N) : gauss_smem<16>(R, N);
+  if (smem > (size_t)kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for the Gaussian tiles");
+  int dev = 0;
+  FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  {
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[dev]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_gauss<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_gauss)");
+      FABF_CUDA(cudaFuncSetAttribute(k_gauss<N, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_gauss)");
+      attr_set[dev] = true;
+    }
+  }
+  const int T = big ? 32 : 16;
+  dim3 g((fa.W + T - 1) / T, (fa.H + T - 1) / T, fa.B);
+  prof_mark(2, st);
+  if (big)
+    k_gauss<N, 32><<<g, kThreads, smem, st>>>(fa, R, nu0);
+  else
+    k_gauss<N, 16><<<g, kThreads, smem, st>>>(fa, R, nu0);
+  ++g_launches;
+  FABF_CUDA(cudaGetLastError(), "k_gauss launch");
+  prof_mark(3, st);
+  k_fallback_gauss<N><<<148 * 4, kThreads, 0, st>>>(fa, R, nu0);
+  ++g_launches;
+  FABF_CUDA(cudaGetLastError(), "k_fallback_gauss launch");
+  prof_mark(4, st);
+  return FABF_OK;
+}
+
 // a fresh set of fallback counters per call
 fabf_status_t fallback_reset(Plan* p, int slots, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int) * (size_t)slots, st), "cudaMemsetAsync(fb_count)");
@@ -2088,6 +2277,57 @@ fabf_status_t fabf_filter_host(fabf_plan_t plan, const float* img, const float* 
   FABF_CUDA(cudaStreamSynchronize(p->cs_out), "cudaStreamSynchronize");
   FABF_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   return FABF_OK;
+}
+
+fabf_status_t fabf_filter_gauss(fabf_plan_t plan, const float* img, const float* theta, const float* sigma,
+                                int rho, int N, float* out, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  if (!p) return fail(FABF_ERR_INVALID_ARGUMENT, "plan is NULL");
+  const int R = 3 * rho;
+  if (rho < 0 || rho > kMaxGaussRho) return fail(FABF_ERR_INVALID_ARGUMENT, "Gaussian omega: 0 <= rho <= 16");
+  fabf_status_t s = validate_filter(p, img, theta, sigma, R, N, out);  // the window is [-3 rho, 3 rho]^2
+  if (s != FABF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  p->last_stream = st;
+  g_launches = 0;
+  struct Record {
+    Plan* p;
+    ~Record() { p->launches = g_launches; }
+  } rec{p};
+  s = fallback_reset(p, 1, st);
+  if (s != FABF_OK) return s;
+  // omega's 1-D factor and sum omega = (sum_d g(d))^2 = nu_0 (eq.(4))
+  double g[2 * 48 + 1] = {}, gs = 0.0;
+  for (int d = -R; d <= R; ++d) gs += (g[d + R] = rho > 0 ? std::exp(-(double)d * d / (2.0 * rho * rho)) : 1.0);
+  FABF_CUDA(cudaMemcpyToSymbolAsync(c_gw, g, sizeof(g), 0, cudaMemcpyHostToDevice, st), "c_gw");
+  s = launch_bounds(p, img, R, p->alpha, p->beta, 0, p->B, 0, (p->H + kBT - 1) / kBT, st);  // step a1 on the box of R
+  if (s != FABF_OK) return s;
+  FilterArgs fa = {};
+  fa.img = img;
+  fa.theta = theta;
+  fa.sigma = sigma;
+  fa.alpha = fa.alpha_w = p->alpha;
+  fa.beta = fa.beta_w = p->beta;
+  fa.out = out;
+  fa.B = p->B;
+  fa.H = p->H;
+  fa.W = p->W;
+  fa.rho = R;
+  fa.flags = p->flags;
+  fa.flag_root = N > 0 ? std::pow(2.0, (double)kFlagBits / N) : 1e300;  // direct (FIR) sums: magnitude 1
+  fa.fb_count = p->fb_count;
+  fa.fb_list = p->fb_list;
+  const float nu0 = (float)(gs * gs);
+  switch (N) {
+#define FABF_GAUSS_CASE(NV) \
+  case NV: s = launch_gauss<NV>(fa, R, nu0, st); break;
+    FABF_GAUSS_CASE(0) FABF_GAUSS_CASE(1) FABF_GAUSS_CASE(2) FABF_GAUSS_CASE(3) FABF_GAUSS_CASE(4)
+    FABF_GAUSS_CASE(5) FABF_GAUSS_CASE(6) FABF_GAUSS_CASE(7) FABF_GAUSS_CASE(8) FABF_GAUSS_CASE(9)
+    FABF_GAUSS_CASE(10)
+#undef FABF_GAUSS_CASE
+    default: return fail(FABF_ERR_UNSUPPORTED, "N > FABF_MAX_N");
+  }
+  return s;
 }
 
 fabf_status_t fabf_filter_mozerov(fabf_plan_t plan, const float* img, const float* theta,

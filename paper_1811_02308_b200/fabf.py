@@ -74,6 +74,9 @@ def lib():
                 L.fabf_sharpen_maps.restype = ctypes.c_int
                 L.fabf_filter_sharpen.argtypes = [P, P, i, i, ctypes.POINTER(_Sharpen), P, P]
                 L.fabf_filter_sharpen.restype = ctypes.c_int
+            if hasattr(L, "fabf_filter_gauss"):
+                L.fabf_filter_gauss.argtypes = [P, P, P, P, i, i, P, P]
+                L.fabf_filter_gauss.restype = ctypes.c_int
             if hasattr(L, "fabf_filter_mozerov"):
                 L.fabf_filter_mozerov.argtypes = [P, P, P, P, i, P, P]
                 L.fabf_filter_mozerov.restype = ctypes.c_int
@@ -344,4 +347,17 @@ def filter_sharpen(plan: Plan, img, rho: int, N: int, out=None, stream=None, **p
     prm = _sharpen_params(params)
     _check(lib().fabf_filter_sharpen(plan.handle, _dev_ptr(img, "img", plan), int(rho), int(N), ctypes.byref(prm),
                                      _dev_ptr(out, "out", plan), _stream_ptr(stream)))
+    return out
+
+
+def filter_gauss(plan: Plan, img, theta, sigma, rho: int, N: int, out=None, stream=None):
+    """fabf_filter_gauss: Algorithm 1 with the Gaussian spatial kernel of eq.(4)
+    on [-3 rho, 3 rho]^2 (device tensors)."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(img)
+    _check(lib().fabf_filter_gauss(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(theta, "theta", plan),
+                                   _dev_ptr(sigma, "sigma", plan), int(rho), int(N), _dev_ptr(out, "out", plan),
+                                   _stream_ptr(stream)))
     return out

@@ -555,3 +555,42 @@ def test_sharpen_application(fb, orc, kind, shape, rho, N, prm):
     mx2, nbad2, _ = compare_guarded(out, o2, 1.0)
     assert nbad2 == 0, f"against the oracle's own maps: max |delta| = {mx2} grey"
     assert plan.last_launch_count() >= 2
+
+
+@pytest.mark.parametrize("kind,shape,rho,N", [
+    ("voronoi", (1, 96, 130), 3, 5), ("texture", (2, 70, 81), 1, 8), ("rect", (1, 100, 100), 5, 2),
+    ("float", (1, 80, 90), 3, 6), ("flat", (1, 40, 40), 2, 5), ("voronoi", (1, 130, 150), 10, 5),
+    ("texture", (1, 140, 160), 12, 4), ("rect", (1, 60, 61), 2, 0), ("voronoi", (1, 64, 64), 0, 3)])
+def test_gaussian_spatial_kernel(fb, orc, kind, shape, rho, N):
+    """NEXT-1: Algorithm 1 with the Gaussian omega of eq.(4) on [-3 rho, 3 rho]^2
+    (fabf_filter_gauss) against the oracle's weighted-histogram reference,
+    every pixel; rho = 12 runs the 16 x 16 tile variant, rho = 0 the identity."""
+    import torch
+
+    w = workloads.random_case(*shape, seed=81 + rho, kind=kind, rho=rho, N=N)
+    plan = fb.Plan(*w.shape)
+    out = fb.filter_gauss(plan, _dev(w.img), _dev(w.theta), _dev(w.sigma), rho, N)
+    torch.cuda.synchronize()
+    o = orc.fast(w.img, w.theta, w.sigma, rho, N, spatial="gauss")
+    mx, nbad, _ = compare_guarded(out.cpu().numpy(), o, grey_scale(w.img))
+    assert nbad == 0, f"max |delta| = {mx} grey ({plan.last_fallback_count()} fallback pixels)"
+
+
+def test_gaussian_spatial_kernel_fallback(fb, orc):
+    """A flat area next to full contrast sends pixels to k_fallback_gauss (exact
+    weighted moments); they match the oracle too."""
+    import torch
+
+    rng = np.random.default_rng(88)
+    f = np.rint(rng.uniform(0, 255, (1, 90, 120)))
+    f[:, :, :50] = np.rint(3 + rng.uniform(0, 2, (1, 90, 50)))
+    f = f.astype(np.float32)
+    th = (f + rng.uniform(-1, 1, f.shape)).astype(np.float32)
+    sg = rng.uniform(0.5, 20, f.shape).astype(np.float32)
+    plan = fb.Plan(*f.shape)
+    out = fb.filter_gauss(plan, _dev(f), _dev(th), _dev(sg), 2, 10)
+    torch.cuda.synchronize()
+    assert plan.last_fallback_count() > 0
+    o = orc.fast(f, th, sg, 2, 10, spatial="gauss")
+    mx, nbad, _ = compare_guarded(out.cpu().numpy(), o, 1.0)
+    assert nbad == 0, f"max |delta| = {mx} grey"
