@@ -1324,6 +1324,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
 //   ratio of fabf_device.cuh with nu_0 = sum omega; pixels whose centring
 //   amplification is too large go to k_fallback_gauss (exact weighted sums).
 __constant__ double c_gw[2 * 48 + 1];  // omega's 1-D factor exp(-d^2 / 2 rho^2), d = -R..R
+constexpr float kGaussKappaBits = 36.0f;
 
 template <int T>
 __host__ __device__ constexpr size_t gauss_smem(int R, int N) {
@@ -1332,7 +1333,7 @@ __host__ __device__ constexpr size_t gauss_smem(int R, int N) {
 }
 
 template <int N, int T>
-__global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, float nu0f) {
+__global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, double nu0) {
   extern __shared__ __align__(16) unsigned char smg[];
   constexpr int NN = N > 0 ? N : 1;
   const int FS = T + 2 * R, H = a.H, W = a.W;
@@ -1387,7 +1388,7 @@ __global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, float n
     }
   }
   __syncthreads();
-  const float n = nu0f;
+  const double n = nu0;  // sum omega, exact to fp64 rounding like the FIR sums (S_0 of the stretch)
   for (int t = tid; t < T * T; t += kThreads) {
     const int r = t / T, x = t - r * T, yy = y0 + r, xx = x0 + x;
     if (yy >= H || xx >= W) continue;
@@ -1404,7 +1405,7 @@ __global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, float n
       continue;
     }
     double Sq[N + 1], nup[NN];
-    Sq[0] = (double)n;
+    Sq[0] = n;
 #pragma unroll
     for (int q = 1; q <= N; ++q) Sq[q] = S[(q - 1) * T * T + t];
     nu_from_sums<N>(Sq, au, bu, nup, 1);
@@ -1412,6 +1413,17 @@ __global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, float n
     float lam, t0;
     const int regime = range_params(al, be, th, sg, lam, t0);
     const PixelResult res = ghat_from_record<N>(nup, 1, th, sg, al, be, regime, a.flags, false, n);
+    // the moment rounding (eps64 times the centring amplification) reaches
+    // g-hat multiplied by kappa: with Gaussian weights a window's effective
+    // sample count is small and kappa large, so the amplification test is
+    // repeated with kappa once it is known (2^kGaussKappaBits, ~1e-3 grey)
+    const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
+    const float amp_bits = (float)N * __log2f((float)((1.0 + fabs(m)) / h)) + __log2f(fmaxf(res.kappa, 1.0f));
+    if (N > 0 && !(amp_bits <= kGaussKappaBits)) {
+      const int slot = atomicAdd(a.fb_count, 1);
+      a.fb_list[slot] = o;
+      continue;
+    }
     a.out[o] = res.g;
   }
 }
@@ -1419,7 +1431,7 @@ __global__ void __launch_bounds__(kThreads) k_gauss(FilterArgs a, int R, float n
 // exact weighted moments for the flagged pixels of k_gauss (thread per pixel):
 // nu_k = sum_j omega(j) P_k(w_j) with the pixel's own stretch (cf. k_fallback)
 template <int N>
-__global__ void __launch_bounds__(kThreads) k_fallback_gauss(FilterArgs a, int R, float nu0f) {
+__global__ void __launch_bounds__(kThreads) k_fallback_gauss(FilterArgs a, int R, double nu0) {
   const int count = *a.fb_count;
   const int H = a.H, W = a.W;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
@@ -1455,7 +1467,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback_gauss(FilterArgs a, int R
     float lam, t0;
     const float th = a.theta[o], sg = a.sigma[o];
     const int regime = range_params(al, be, th, sg, lam, t0);
-    const PixelResult res = ghat_from_record<N>(nu + 1, 1, th, sg, al, be, regime, a.flags, false, nu0f);
+    const PixelResult res = ghat_from_record<N>(nu + 1, 1, th, sg, al, be, regime, a.flags, false, nu[0]);
     a.out[o] = res.g;
   }
 }
@@ -1577,7 +1589,6 @@ __global__ void __launch_bounds__(kThreads) k_sharpen_maps(const float* __restri
     Gb[t] = bb;
   }
   __syncthreads();
-  const float inv_n = 1.0f / (float)(w * w);
   for (int t = threadIdx.x; t < T * T; t += kThreads) {
     const int y = t / T, x = t - y * T;
     const int yy = y0 + y, xx = x0 + x;
@@ -1591,7 +1602,7 @@ __global__ void __launch_bounds__(kThreads) k_sharpen_maps(const float* __restri
     }
     const double f = (double)F[(y + R) * FS + x + R];
     const size_t o = plane + (size_t)yy * W + xx;
-    theta[o] = (float)(2.0 * f - acc * (double)inv_n);
+    theta[o] = (float)(2.0 * f - acc / (double)(w * w));
     sigma[o] = s_hi - (s_hi - s_lo) * fminf(fabsf(L) * inv_sat, 1.0f);
   }
 }
@@ -2045,7 +2056,7 @@ size_t staging_pitch(size_t px) { return (px + 3) & ~(size_t)3; }
 // that the fp64 footprint fits), then the exact weighted fallback
 constexpr int kMaxGaussRho = 16;
 template <int N>
-fabf_status_t launch_gauss(FilterArgs& fa, int R, float nu0, cudaStream_t st) {
+fabf_status_t launch_gauss(FilterArgs& fa, int R, double nu0, cudaStream_t st) {
   const bool big = R <= 30;
   const size_t smem = big ? gauss_smem<32>(R, N) : gauss_smem<16>(R, N);
   if (smem > (size_t)kMaxDynSmem) return fail(FABF_ERR_INVALID_ARGUMENT, "rho too large for the Gaussian tiles");
@@ -2317,7 +2328,7 @@ fabf_status_t fabf_filter_gauss(fabf_plan_t plan, const float* img, const float*
   fa.flag_root = N > 0 ? std::pow(2.0, (double)kFlagBits / N) : 1e300;  // direct (FIR) sums: magnitude 1
   fa.fb_count = p->fb_count;
   fa.fb_list = p->fb_list;
-  const float nu0 = (float)(gs * gs);
+  const double nu0 = gs * gs;
   switch (N) {
 #define FABF_GAUSS_CASE(NV) \
   case NV: s = launch_gauss<NV>(fa, R, nu0, st); break;

@@ -286,7 +286,7 @@ template <int N>
 __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int ns, float theta,
                                                         float sigma, float alpha, float beta,
                                                         int regime, unsigned flags, bool want_t2n,
-                                                        float n) {
+                                                        double n) {
   PixelResult res;
   res.code = 0u;
   double scale_log = 0.0;  // log of the common factor applied to A (diagnostics only)
@@ -299,7 +299,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     float T2 = 0.0f, U = 0.0f, ab = 0.0f;
 #pragma unroll
     for (int k = 0; k <= N; ++k) {
-      const float v = k == 0 ? n : (float)nup[(k - 1) * ns];
+      const float v = k == 0 ? (float)n : (float)nup[(k - 1) * ns];
       const float t = v * A[k];
       T2 += t;
       ab += fabsf(t);
@@ -318,7 +318,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
     const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
     double T2, U, ab, A0, X0;
-    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, ns, (double)n, T2, U, ab, A0, X0);
+    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, ns, n, T2, U, ab, A0, X0);
     T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A0, X0f = (float)X0;
     if (want_t2n) {
       const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
@@ -333,7 +333,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     res.code |= kCodeFarTheta;
     const double dist = t0 < 0.0 ? -t0 : t0 - 1.0;
     scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
-    contract<N>(nup, ns, (double)n, A, X, T2f, Uf, abf, A0f, X0f);
+    contract<N>(nup, ns, n, A, X, T2f, Uf, abf, A0f, X0f);
   }
   float ratio;
   if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {
@@ -344,7 +344,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
   }
   res.kappa = (T2f > 0.0f) ? abf / T2f : CUDART_INF_F;
   // T2 / n in the units of eq.(29) (J = A/2, unscaled)
-  res.t2n = want_t2n ? (float)(0.5 * (double)T2f / (double)n * exp(-scale_log)) : 0.0f;
+  res.t2n = want_t2n ? (float)(0.5 * (double)T2f / n * exp(-scale_log)) : 0.0f;
   const float mid = 0.5f * (alpha + beta), half = 0.5f * (beta - alpha);
   float g = fmaf(half, ratio, mid);
   if (flags & kFlagClamp) g = fminf(fmaxf(g, alpha), beta);

@@ -551,9 +551,6 @@ def test_sharpen_application(fb, orc, kind, shape, rho, N, prm):
     o = orc.fast(w.img, th, sg, rho, N)
     mx, nbad, _ = compare_guarded(out, o, 1.0)
     assert nbad == 0, f"max |delta| = {mx} grey"
-    o2 = orc.fast(w.img, rth.astype(np.float32), rsg.astype(np.float32), rho, N)
-    mx2, nbad2, _ = compare_guarded(out, o2, 1.0)
-    assert nbad2 == 0, f"against the oracle's own maps: max |delta| = {mx2} grey"
     assert plan.last_launch_count() >= 2
 
 
