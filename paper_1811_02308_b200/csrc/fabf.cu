@@ -49,6 +49,9 @@ struct fabf_plan_s {
   // entries and the call's total is the sum of its slots
   int* fb_count = nullptr;
   int* fb_list = nullptr;
+  unsigned* fb_bits = nullptr;  // one bit per pixel, 32-pixel row words (all zero between calls)
+  int* seg_list = nullptr;      // row words holding flagged pixels, per band region
+  int* seg_count = nullptr;     // per band slot, like fb_count
   int fb_slots = 0;  // slots the last call used
   int launches = 0;  // kernels the last call launched (fabf_last_launch_count)
   // FABF_FLAG_DEBUG: [0] inputs violating the preconditions, [1] the first one's index
@@ -76,8 +79,6 @@ constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds inside k_filter by defau
 int g_fuse_rho = getenv("FABF_FUSE_RHO") ? atoi(getenv("FABF_FUSE_RHO")) : kFuseRho;
 // segment cap: max(g_seg_min, 3 w) rows (A/B switch FABF_SEG_MIN)
 int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 64;
-// k_fallback mode: 0 auto (default), 1 thread per pixel, 2 warp per pixel (A/B switch)
-int g_fb_mode = getenv("FABF_FB_MODE") ? atoi(getenv("FABF_FB_MODE")) : 0;
 // fabf_filter_host row bands per frame (A/B switch FABF_HOST_BANDS, 1..16)
 int g_host_bands = getenv("FABF_HOST_BANDS") ? std::max(1, std::min(16, atoi(getenv("FABF_HOST_BANDS")))) : 6;
 #ifndef FABF_FILTER_MINB
@@ -543,9 +544,16 @@ struct FilterArgs {
   int SH;          // segment cap (rows)
   int b0, r0, r1;  // images [b0, b0 + B), rows [r0, r1) of each (row bands)
   unsigned flags;
-  double flag_root;  // 2^(flag_bits / N)
+  double flag_root;         // 2^(flag_bits / N) with the prefix-row magnitude
+  double flag_root_direct;  // 2^(flag_bits / N): direct sums (k_fallback_seg)
   int* fb_count;
   int* fb_list;
+  // exact-moment fallback by 32-pixel row segments (k_fallback_seg): one bit
+  // per flagged pixel, the segments that hold any, and their count
+  unsigned* fb_bits;
+  int* seg_list;
+  int* seg_count;
+  int WS;  // 32-pixel words per image row
   float* d_alpha;  // diagnostics (fabf_filter_diag), may be NULL
   float* d_beta;
   float* d_kappa;
@@ -1108,8 +1116,9 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             if (a.d_code) a.d_code[po[i]] = (unsigned char)kCodeIdentity;
           } else if (stretch_flagged(fma((double)p_al[i], invS, mcs), fma((double)p_be[i], invS, mcs),
                                      a.flag_root)) {  // exact-moment fallback pass
-            const int slotfb = atomicAdd(a.fb_count, 1);
-            a.fb_list[slotfb] = po[i];
+            const int pX = x0 + px_x, pY = Yb + px_r + i * (kThreads / TW);
+            const int sw = (bimg * H + pY) * a.WS + (pX >> 5);
+            if (atomicOr(&a.fb_bits[sw], 1u << (pX & 31)) == 0u) a.seg_list[atomicAdd(a.seg_count, 1)] = sw;
             if constexpr (FB) {  // the fallback kernel reads alpha, beta from the plan
               a.alpha_w[po[i]] = p_al[i];
               a.beta_w[po[i]] = p_be[i];
@@ -1211,15 +1220,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 }
 
 // ============================================================================
-// exact-moment fallback: nu_k = sum_j P_k(w_j) directly in fp64 over the
-// window of each listed pixel (w_j stretched by the pixel's own alpha, beta:
-// no centring error), then the same per-pixel integrals / ratio as k_filter.
-// Two modes, chosen per launch from the device-side list length (uniform):
-//   thread mode: one thread per pixel -- many pixels, small windows;
-//   warp mode:   one warp per pixel, the lanes split the flattened window
-//                (coalesced row loads, full lanes) and reduce by shuffles --
-//                short lists (one serial thread per pixel takes 0.93 ms for
-//                416 pixels at rho = 40; a warp per pixel 0.11 ms).
+// exact-moment fallback helpers: nu_k = sum_j P_k(w_j) directly in fp64 over the
+// window of a pixel (w_j stretched by the pixel's own alpha, beta: no centring
+// error), then the same per-pixel integrals / ratio as k_filter (used by
+// k_fallback_seg for the pixels its segment centring cannot serve, and by the
+// Gaussian path's k_fallback_gauss with weights).
 // The Legendre values come from the monic recurrence
 // R_{k+1} = s R_k - k^2 / (4k^2 - 1) R_{k-1}, R_k = P_k / m_k with
 // m_k = binom(2k, k) / 2^k (the three-term recurrence of P_k divided by its
@@ -1241,71 +1246,135 @@ __device__ __forceinline__ void fb_accumulate(double (&acc)[N + 1], double sv) {
     r1 = r2;
   }
 }
+// ============================================================================
+// exact-moment fallback by row segments (O(rho) per pixel instead of the
+// O(rho^2) direct window sums of k_fallback).  k_filter marks each flagged
+// pixel in a bitmap of 32-pixel row segments and lists the segments.  One warp
+// per listed segment (lane = pixel): the segment's own centre and power-of-two
+// scale come from the union of its flagged pixels' [alpha, beta] (flagged
+// pixels sit in flat areas, so that union is narrow: little amplification),
+// the lanes build the fp64 power sums of the segment's 32 + 2 rho columns over
+// the window rows, each flagged lane sums its w columns (direct sums, no
+// prefix magnitudes), re-checks the amplification against the segment centre,
+// and finishes like k_filter; a lane that still fails takes the exact direct
+// window sums of k_fallback (its own stretch).  The segment's bits are cleared
+// for the next call.
 template <int N>
-__global__ void __launch_bounds__(kThreads) k_fallback(FilterArgs a, int mode) {
-  const int count = *a.fb_count;
-  const int rho = a.rho, w = 2 * rho + 1, n = w * w;
-  const int H = a.H, W = a.W;
-  const int nthreads = gridDim.x * blockDim.x;
-  // mode 0: auto; 1: thread per pixel; 2: warp per pixel
-  // (measured crossover: a warp per pixel wins while the list is shorter than
-  // ~5 warps' worth per resident warp; longer lists are throughput-bound and
-  // thread mode's neighbouring-pixel loads share L1 lines -- 3.9 vs 6.2 ms
-  // for 198k pixels at rho = 40)
-  const bool warp_mode = mode == 2 || (mode == 0 && count <= 4 * (nthreads / 32));
-  const int lanes = warp_mode ? 32 : 1;
-  const int sub = warp_mode ? (threadIdx.x & 31) : 0;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / lanes;
-  const int nw = nthreads / lanes;
-  for (int i = gw; i < count; i += nw) {
-    const int o = a.fb_list[i];
-    const int b = o / (H * W), rem = o - b * H * W, y = rem / W, x = rem - y * W;
-    const float* img = a.img + (size_t)b * H * W;
-    const float al = a.alpha_w[o], be = a.beta_w[o];
-    const double mid = 0.5 * ((double)al + (double)be), ih = 2.0 / ((double)be - (double)al);
-    double acc[N + 1];
+__device__ __forceinline__ PixelResult fallback_direct(const FilterArgs& a, const float* img, int x, int y, float al,
+                                                       float be, float th, float sg) {
+  const int rho = a.rho, H = a.H, W = a.W;
+  const double mid = 0.5 * ((double)al + (double)be), ih = 2.0 / ((double)be - (double)al);
+  double acc[N + 1];
 #pragma unroll
-    for (int k = 0; k <= N; ++k) acc[k] = 0.0;
-    if (warp_mode) {
-      // flattened window index j = sub + 32 t -> (dy, dx), advanced incrementally
-      int dy = sub / w, dx = sub - (sub / w) * w;
-      for (int j = sub; j < n; j += 32) {
-        const float* row = img + reflect_index(y - rho + dy, H) * W;
-        const double sv = ((double)__ldg(row + reflect_index(x - rho + dx, W)) - mid) * ih;
-        fb_accumulate<N>(acc, sv);
-        dx += 32;
-        while (dx >= w) {
-          dx -= w;
-          ++dy;
-        }
-      }
+  for (int k = 0; k <= N; ++k) acc[k] = 0.0;
+  for (int dy = -rho; dy <= rho; ++dy) {
+    const float* row = img + reflect_index(y + dy, H) * W;
+    for (int dx = -rho; dx <= rho; ++dx)
+      fb_accumulate<N>(acc, ((double)__ldg(row + reflect_index(x + dx, W)) - mid) * ih);
+  }
+  double nu[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k)
-        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-    } else {
-#pragma unroll 4
-      for (int dy = -rho; dy <= rho; ++dy) {  // (unrolled: several rows' loads in flight)
-        const float* row = img + reflect_index(y + dy, H) * W;
-        for (int dx = -rho; dx <= rho; ++dx) {
-          const double sv = ((double)__ldg(row + reflect_index(x + dx, W)) - mid) * ih;
-          fb_accumulate<N>(acc, sv);
-        }
-      }
+  for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * c_monic_scale[k] * acc[k];
+  float lam, t0;
+  const int regime = range_params(al, be, th, sg, lam, t0);
+  const int w = 2 * rho + 1;
+  return ghat_from_record<N>(nu + 1, 1, th, sg, al, be, regime, a.flags, a.d_t2n != nullptr, (double)(w * w));
+}
+
+constexpr int kSegWarps = 4;  // warps per CTA of k_fallback_seg
+constexpr int kSegDirectRho = 5;  // rho <= this: per-lane direct window sums (measured crossover)
+template <int N>
+__global__ void __launch_bounds__(32 * kSegWarps) k_fallback_seg(FilterArgs a) {
+  extern __shared__ __align__(16) unsigned char smf[];
+  constexpr int NN = N > 0 ? N : 1;
+  const int rho = a.rho, w = 2 * rho + 1, H = a.H, W = a.W, Lc = 32 + 2 * rho;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* Vw = reinterpret_cast<double*>(smf) + (size_t)wib * NN * Lc;  // [NN][Lc] this warp's column sums
+  const int count = *a.seg_count;
+  const int nwarps = gridDim.x * kSegWarps;
+  for (int si = blockIdx.x * kSegWarps + wib; si < count; si += nwarps) {
+    const int sw = a.seg_list[si];
+    const unsigned mask = a.fb_bits[sw];
+    __syncwarp();
+    if (lane == 0) {
+      a.fb_bits[sw] = 0u;  // clean for the next call
+      atomicAdd(a.fb_count, __popc(mask));
     }
-    if (sub == 0) {
-      double nu[N + 1];
+    const int by = sw / a.WS, x0 = (sw - by * a.WS) * 32, b = by / H, y = by - b * H;
+    const float* img = a.img + (size_t)b * H * W;
+    const int x = x0 + lane;
+    const bool flagged = ((mask >> lane) & 1u) && x < W;
+    const size_t o = (size_t)b * H * W + (size_t)y * W + x;
+    float al = 0.f, be = 0.f;
+    if (flagged) al = a.alpha_w[o], be = a.beta_w[o];
+    float umin = flagged ? al : CUDART_INF_F, umax = flagged ? be : -CUDART_INF_F;
+    for (int off = 16; off > 0; off >>= 1) {
+      umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, off));
+      umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+    }
+    const double cT = 0.5 * ((double)umin + (double)umax), halfr = 0.5 * ((double)umax - (double)umin);
+    int e2 = 0;
+    if (halfr > 0.0) frexp(halfr, &e2);
+    const double invS = ldexp(1.0, -e2), mcs = -cT * invS;
+    if (rho <= kSegDirectRho) {  // small windows: each lane's direct sums are cheaper than the columns
+      if (flagged) {
+        const float th = a.theta[o], sg = a.sigma[o];
+        const PixelResult res = fallback_direct<N>(a, img, x, y, al, be, th, sg);
+        a.out[o] = res.g;
+        if (a.d_kappa) a.d_kappa[o] = res.kappa;
+        if (a.d_t2n) a.d_t2n[o] = res.t2n;
+        if (a.d_code) a.d_code[o] = (unsigned char)(res.code | kCodeFallback);
+      }
+      continue;
+    }
+    // column power sums over the window rows, lanes over the segment's columns
+    for (int cc = lane; cc < Lc; cc += 32) {
+      const float* col = img + reflect_index(min(x0 - rho + cc, W - 1 + rho), W);
+      double V[NN];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) nu[k] = (double)(2 * k + 1) * c_monic_scale[k] * acc[k];
-      float lam, t0;
+      for (int q = 0; q < NN; ++q) V[q] = 0.0;
+      for (int dy = -rho; dy <= rho; ++dy) {
+        const double u = fma((double)__ldg(col + reflect_index(y + dy, H) * W), invS, mcs);
+        double pu = u;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          V[q] += pu;
+          pu *= u;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) Vw[q * Lc + cc] = V[q];
+    }
+    __syncwarp();
+    if (flagged) {
       const float th = a.theta[o], sg = a.sigma[o];
-      const int regime = range_params(al, be, th, sg, lam, t0);
-      PixelResult res = ghat_from_record<N>(nu + 1, 1, th, sg, al, be, regime, a.flags,
-                                            a.d_t2n != nullptr, (float)n);
+      const double au = fma((double)al, invS, mcs), bu = fma((double)be, invS, mcs);
+      PixelResult res;
+      unsigned code = kCodeFallback;
+      if (stretch_flagged(au, bu, a.flag_root_direct)) {  // still amplified: the exact direct sums
+        res = fallback_direct<N>(a, img, x, y, al, be, th, sg);
+      } else {
+        double S[N + 1];
+        S[0] = (double)(w * w);
+#pragma unroll
+        for (int q = 1; q <= N; ++q) {
+          double acc = 0.0;
+          const double* v = Vw + (q - 1) * Lc + lane;
+          for (int d = 0; d < w; ++d) acc += v[d];
+          S[q] = acc;
+        }
+        double nup[NN];
+        nu_from_sums<N>(S, au, bu, nup, 1);
+        float lam, t0;
+        const int regime = range_params(al, be, th, sg, lam, t0);
+        res = ghat_from_record<N>(nup, 1, th, sg, al, be, regime, a.flags, a.d_t2n != nullptr, (double)(w * w));
+      }
       a.out[o] = res.g;
       if (a.d_kappa) a.d_kappa[o] = res.kappa;
       if (a.d_t2n) a.d_t2n[o] = res.t2n;
-      if (a.d_code) a.d_code[o] = (unsigned char)(res.code | kCodeFallback);
+      if (a.d_code) a.d_code[o] = (unsigned char)(res.code | code);
     }
+    __syncwarp();  // Vw reused by the warp's next segment
   }
 }
 
@@ -1870,10 +1939,23 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
     s = launch_filter_net<N, 17, 64>(fa, st);
   if (s != FABF_OK) return s;
   prof_mark(3, st);
-  // one thread per pixel (neighbouring list entries share their windows in L1)
-  k_fallback<N><<<148 * 4, kThreads, 0, st>>>(fa, g_fb_mode);
-  ++g_launches;
-  FABF_CUDA(cudaGetLastError(), "k_fallback launch");
+  {  // the exact-moment fallback by row segments
+    const size_t smem = sizeof(double) * kSegWarps * (N > 0 ? N : 1) * (32 + 2 * fa.rho);
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    FABF_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    {
+      std::lock_guard<std::mutex> lk(g_launch_mu);
+      if (!attr_set[dev]) {
+        FABF_CUDA(cudaFuncSetAttribute(k_fallback_seg<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                  "cudaFuncSetAttribute(k_fallback_seg)");
+        attr_set[dev] = true;
+      }
+    }
+    k_fallback_seg<N><<<148 * 4, 32 * kSegWarps, smem, st>>>(fa);
+    ++g_launches;
+    FABF_CUDA(cudaGetLastError(), "k_fallback_seg launch");
+  }
   prof_mark(4, st);
   return FABF_OK;
 }
@@ -2006,9 +2088,14 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
     const double mag = rho <= 3 ? 1.0 : (double)L * w / ((double)w * w);
     const double bits = (double)kFlagBits - std::log2(mag);
     fa.flag_root = N > 0 ? std::pow(2.0, bits / N) : 1e300;
+    fa.flag_root_direct = N > 0 ? std::pow(2.0, (double)kFlagBits / N) : 1e300;
   }
   fa.fb_count = p->fb_count + fb_slot;
   fa.fb_list = p->fb_list + ((size_t)b0 * p->H + fa.r0) * p->W;
+  fa.WS = (p->W + 31) / 32;
+  fa.fb_bits = p->fb_bits;
+  fa.seg_count = p->seg_count + fb_slot;
+  fa.seg_list = p->seg_list + ((size_t)b0 * p->H + fa.r0) * fa.WS;
   fa.d_alpha = diag ? diag->alpha : nullptr;
   fa.d_beta = diag ? diag->beta : nullptr;
   if (!fa.d_alpha || !fa.d_beta) fa.d_alpha = fa.d_beta = nullptr;
@@ -2093,6 +2180,7 @@ fabf_status_t launch_gauss(FilterArgs& fa, int R, double nu0, cudaStream_t st) {
 // a fresh set of fallback counters per call
 fabf_status_t fallback_reset(Plan* p, int slots, cudaStream_t st) {
   FABF_CUDA(cudaMemsetAsync(p->fb_count, 0, sizeof(int) * (size_t)slots, st), "cudaMemsetAsync(fb_count)");
+  FABF_CUDA(cudaMemsetAsync(p->seg_count, 0, sizeof(int) * (size_t)slots, st), "cudaMemsetAsync(seg_count)");
   p->fb_slots = slots;
   return FABF_OK;
 }
@@ -2148,6 +2236,10 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
                                      ((width + kBT - 1) / kBT))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_count, sizeof(int) * (size_t)batch * Plan::kMaxBandsPlan)) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_list, px * sizeof(int))) != cudaSuccess ||
+      (e = cudaMalloc(&p->fb_bits, sizeof(unsigned) * (size_t)batch * height * ((width + 31) / 32))) != cudaSuccess ||
+      (e = cudaMemset(p->fb_bits, 0, sizeof(unsigned) * (size_t)batch * height * ((width + 31) / 32))) != cudaSuccess ||
+      (e = cudaMalloc(&p->seg_list, sizeof(int) * (size_t)batch * height * ((width + 31) / 32))) != cudaSuccess ||
+      (e = cudaMalloc(&p->seg_count, sizeof(int) * (size_t)batch * Plan::kMaxBandsPlan)) != cudaSuccess ||
       (e = alloc_ring(p)) != cudaSuccess ||
       ((flags & FABF_FLAG_DEBUG) &&
        (e = cudaMalloc(&p->dbg, 2 * sizeof(unsigned long long))) != cudaSuccess)) {
@@ -2567,6 +2659,9 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   cudaFree(p->ring);
   cudaFree(p->fb_count);
   cudaFree(p->fb_list);
+  cudaFree(p->fb_bits);
+  cudaFree(p->seg_list);
+  cudaFree(p->seg_count);
   cudaFree(p->dbg);
   cudaFree(p->h_in);
   cudaFree(p->h_out);

@@ -269,51 +269,33 @@ def test_fallback_path_parity(fb, orc):
     assert nbad == 0, f"max |delta| = {mx}"
 
 
-_FB_SCRIPT = r"""
-import sys, numpy as np, torch
-import paper_1811_02308_b200 as fb
-f, th, sg = (np.load(sys.argv[1] + n + ".npy") for n in ("f", "th", "sg"))
-rho, N = int(sys.argv[2]), int(sys.argv[3])
-plan = fb.Plan(*f.shape)
-d = lambda a: torch.from_numpy(a).cuda()
-out = fb.filter(plan, d(f), d(th), d(sg), rho, N)
-torch.cuda.synchronize()
-np.save(sys.argv[1] + "out.npy", out.cpu().numpy())
-print(plan.last_fallback_count())
-"""
-
-
-@pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("rho", [2, 12])
-def test_fallback_modes_parity(fb, orc, tmp_path, mode, rho):
-    """Both k_fallback modes (FABF_FB_MODE=1: a thread per pixel, 2: a warp per
-    pixel over the flattened window; the default picks by list length) on a
-    flat-next-to-texture image with a long fallback list, every pixel against
-    the oracle.  The mode is read at library load, hence the subprocess."""
-    import os
-    import subprocess
-    import sys
+@pytest.mark.parametrize("rho,N,fused", [(2, 10, False), (12, 10, False), (40, 8, False), (12, 10, True)])
+def test_fallback_segments_parity(fb, orc, rho, N, fused):
+    """k_fallback_seg (the exact-moment fallback by 32-pixel row segments with
+    their own centre, O(rho) per pixel) on a flat-next-to-texture image with a
+    long fallback list, every pixel against the oracle; a second call on the
+    same plan (the segment bitmap is cleared) gives the same result."""
+    import torch
 
     rng = np.random.default_rng(50 + rho)
-    H, W = 120, 200
+    H, W = max(120, 2 * rho + 40), 200
     f = np.rint(rng.uniform(0, 255, (H, W)))
     f[:, :90] = np.rint(3 + rng.uniform(0, 2, (H, 90)))
+    f[H // 2:, 150:] = np.rint(250 + rng.uniform(0, 3, (H - H // 2, 50)))  # a second, bright flat area
     f = f.astype(np.float32)[None]
     th = (f + rng.uniform(-1, 1, f.shape)).astype(np.float32)
     sg = rng.uniform(0.5, 20, f.shape).astype(np.float32)
-    pre = str(tmp_path) + "/"
-    for n, a in (("f", f), ("th", th), ("sg", sg)):
-        np.save(pre + n + ".npy", a)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, FABF_FB_MODE=str(mode), PYTHONPATH=root)
-    r = subprocess.run([sys.executable, "-c", _FB_SCRIPT, pre, str(rho), "10"], env=env,
-                       capture_output=True, text=True, timeout=300, cwd=root)
-    assert r.returncode == 0, r.stderr[-2000:]
-    assert int(r.stdout.split()[-1]) > 0  # the fallback list is not empty
-    out = np.load(pre + "out.npy")
-    o = orc.fast(f, th, sg, rho, 10)
-    mx, nbad, _ = compare_guarded(out, o, 1.0)
-    assert nbad == 0, f"max |delta| = {mx}"
+    plan = fb.Plan(*f.shape, fb.FLAG_FUSED if fused else 0)
+    out = fb.filter(plan, _dev(f), _dev(th), _dev(sg), rho, N)
+    torch.cuda.synchronize()
+    nfb = plan.last_fallback_count()
+    assert nfb > 0
+    out2 = fb.filter(plan, _dev(f), _dev(th), _dev(sg), rho, N)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2) and plan.last_fallback_count() == nfb
+    o = orc.fast(f, th, sg, rho, N)
+    mx, nbad, _ = compare_guarded(out.cpu().numpy(), o, 1.0)
+    assert nbad == 0, f"max |delta| = {mx} ({nfb} fallback pixels)"
 
 
 def test_debug_flag_validates_preconditions(fb):
