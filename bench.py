@@ -128,10 +128,11 @@ def alg_fp64_flops_per_pixel(N: int, share_fp64_j: float, share_identity: float 
 
 def _ncu_summary(kernel: str):
     """Executed-pipe figures of ``kernel`` from the committed ncu --set full
-    summary (profiles/ncu_summary.json, written by tools/ncu_summary.py), or {}."""
+    capture summary (profiles/traffic.json, written by tools/ncu_traffic.py), or {}."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f).get(kernel, {})
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f).get(kernel, {})
+        return dict(d, source=d.get("report"))
     except Exception:
         return {}
 

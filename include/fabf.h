@@ -58,8 +58,9 @@ typedef enum {
 #define FABF_FLAG_FUSED 0x8u   /* compute the bounds alpha, beta (step a1) inside the per-pixel
                                   kernel for every rho (one kernel reads f, theta, sigma and
                                   writes g-hat: north_star (e)).  Without it they are
-                                  fused for rho <= 5 and produced by a separate bounds kernel
-                                  for larger rho, the faster choice on B200. */
+                                  computed inside the kernel only for rho <= 5 on calls of at
+                                  most 2^21 pixels and by a separate bounds kernel otherwise,
+                                  the faster choice on B200.                 */
 
 /* per-pixel diagnostic code bits (fabf_diag_t.code) */
 #define FABF_CODE_IDENTITY 0x1u /* alpha == beta: g-hat = f(i)                               */

@@ -75,7 +75,12 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxBands = fabf_plan_s::kMaxBandsPlan;  // fabf_filter_host row bands
-constexpr int kFuseRho = 5;  // rho <= kFuseRho: bounds inside k_filter by default
+// bounds inside k_filter by default for rho <= kFuseRho on calls of at most
+// kFusePixels pixels (configs 1-2: one launch less outweighs the dearer
+// in-kernel bounds); the separate bounds kernel elsewhere (faster at every rho
+// of configs 3-5); FABF_FLAG_FUSED plans always fuse.
+constexpr int kFuseRho = 5;
+constexpr long long kFusePixels = 1LL << 21;
 int g_fuse_rho = getenv("FABF_FUSE_RHO") ? atoi(getenv("FABF_FUSE_RHO")) : kFuseRho;
 // segment cap: max(g_seg_min, 3 w) rows (A/B switch FABF_SEG_MIN)
 int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 64;
@@ -2024,12 +2029,13 @@ fabf_status_t validate_filter(Plan* p, const float* img, const float* theta, con
 }
 
 // where the bounds run: FABF_FLAG_FUSED plans always in k_filter; otherwise
-// in k_filter for rho <= g_fuse_rho (default kFuseRho: measured crossover,
-// DESIGN.md section 4), else in k_bounds.  FABF_FUSE_RHO overrides the
+// in k_filter for rho <= g_fuse_rho (default kFuseRho) on small calls
+// (<= kFusePixels), else in k_bounds.  FABF_FUSE_RHO overrides the rho
 // crossover (experiments).
 bool fused_choice(const Plan* p, int rho) {
   if (p->flags & FABF_FLAG_FUSED) return true;
-  return rho <= g_fuse_rho && p->ring_elems >= ring_elems_per_cta(rho);
+  return rho <= g_fuse_rho && (long long)p->B * p->H * p->W <= kFusePixels &&
+         p->ring_elems >= ring_elems_per_cta(rho);
 }
 
 // The three kernels for images [b0, b0 + nb), rows [64 ty0, min(H, 64 ty1)).

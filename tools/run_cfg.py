@@ -8,7 +8,7 @@ import workloads
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 w = workloads.config(cfg)
-plan = fb.Plan(*w.shape)
+plan = fb.Plan(*w.shape, int(os.environ.get("QFLAGS", "0")))
 d = lambda a: torch.from_numpy(a).cuda()
 img, th, sg = d(w.img), d(w.theta), d(w.sigma)
 out = torch.empty_like(img)
