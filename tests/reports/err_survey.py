@@ -2,14 +2,14 @@
 of cases (GPU box): max / p99.9 error in grey levels, counts above 0.01 and
 0.025, and the worst pixels with their kappa, lambda, t0 and regime code.
 
-  python tools/err_survey.py [quick]
+  python tests/reports/err_survey.py [quick]
 """
 import json
 import os
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np
 import torch
 

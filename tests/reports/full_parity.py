@@ -1,5 +1,5 @@
 """Every pixel of a full-size BASELINE config against the oracle (GPU box;
-minutes of CPU for the oracle):  python tools/full_parity.py 4 > profiles/r1_full_parity_cfg4.json
+minutes of CPU for the oracle):  python tests/reports/full_parity.py 4 > profiles/r1_full_parity_cfg4.json
 
 Reports max |delta| (grey), the count above 0.01 / 0.05, the bit-exactness of
 alpha / beta (fabf_bounds vs the oracle's window scan) and the identity pixels."""
@@ -8,8 +8,8 @@ import os
 import sys
 import time
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np
 import torch
 

@@ -9,14 +9,14 @@
   (literal / guarded / guarded + clamp) -- the paper's 40 dB bar (P:516-518);
 * the paper's context: MATLAB 9.1 on a 3.4 GHz CPU, Table II.
 
-GPU box:  python tools/oracle_report.py > profiles/r2_oracle_report.jsonl
+GPU box:  python tests/reports/oracle_report.py > profiles/r2_oracle_report.jsonl
 """
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 
 import oracle

@@ -3,14 +3,14 @@ fabfo_brute) per BASELINE config, three ways: literal eq.(29), guarded
 (reading R7), guarded + clamp (north_star acceptance: "PSNR of the fast output
 against brute force reported per config").  GPU box:
 
-  python tools/psnr_report.py > profiles/r1_psnr.jsonl
+  python tests/reports/psnr_report.py > profiles/r1_psnr.jsonl
 """
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

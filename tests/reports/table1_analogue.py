@@ -8,13 +8,13 @@ stand in; the paper's omega is a Gaussian on [-3 rho, 3 rho]^2, ours the box
 of half-width rho (reading R1), so the rho columns are not the same windows.
 The GPU path computes g-hat; the oracle computes brute force.  GPU box:
 
-  python tools/table1_analogue.py > profiles/r2_table1_analogue.jsonl
+  python tests/reports/table1_analogue.py > profiles/r2_table1_analogue.jsonl
 """
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

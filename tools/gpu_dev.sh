@@ -3,7 +3,7 @@
 # per-stage timing of config 4 for every library given in LIBS
 mkdir -p gpurun_out
 TAG=${TAG:-dev}
-FABF_LIB=${CHECK_LIB:-$PWD/vlibs/libfabf_dev.so} timeout 900 python tools/quick_check.py > gpurun_out/quick_$TAG.log 2>&1
+FABF_LIB=${CHECK_LIB:-$PWD/vlibs/libfabf_dev.so} timeout 900 python tests/reports/quick_check.py > gpurun_out/quick_$TAG.log 2>&1
 echo "exit $?" >> gpurun_out/quick_$TAG.log
 for lib in ${LIBS:-vlibs/libfabf_dev.so}; do
   for c in ${CFGS:-4}; do
