@@ -83,7 +83,7 @@ constexpr int kFuseRho = 5;
 constexpr long long kFusePixels = 1LL << 21;
 int g_fuse_rho = getenv("FABF_FUSE_RHO") ? atoi(getenv("FABF_FUSE_RHO")) : kFuseRho;
 // segment cap: max(g_seg_min, 3 w) rows (A/B switch FABF_SEG_MIN)
-int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 64;
+int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 256;
 // fabf_filter_host row bands per frame (A/B switch FABF_HOST_BANDS, 1..16)
 int g_host_bands = getenv("FABF_HOST_BANDS") ? std::max(1, std::min(16, atoi(getenv("FABF_HOST_BANDS")))) : 6;
 #ifndef FABF_FILTER_MINB
@@ -104,6 +104,23 @@ thread_local int g_launches = 0;  // kernels launched by the current entry point
 fabf_status_t fail(fabf_status_t s, const std::string& msg) {
   g_last_error = msg;
   return s;
+}
+
+// PDL launches of k_filter / k_fallback_seg (FABF_PDL=0 turns them off: A/B)
+bool g_pdl = !(getenv("FABF_PDL") && atoi(getenv("FABF_PDL")) == 0);
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 fabf_status_t cuda_fail(cudaError_t e, const char* what) {
@@ -178,6 +195,11 @@ fabf_status_t ensure_tables(int dev) {
   FABF_CUDA(cudaMemcpyToSymbol(c_glB_W, bW, sizeof(bW)), "cudaMemcpyToSymbol(c_glB_W)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glC_x, xc.data(), sizeof(double) * kGlC), "cudaMemcpyToSymbol(c_glC_x)");
   FABF_CUDA(cudaMemcpyToSymbol(c_glC_w, wc.data(), sizeof(double) * kGlC), "cudaMemcpyToSymbol(c_glC_w)");
+  {
+    double e2[64];
+    for (int j = 0; j < 64; ++j) e2[j] = (double)exp2l((long double)j / 64.0L);
+    FABF_CUDA(cudaMemcpyToSymbol(c_exp2_64, e2, sizeof(e2)), "cudaMemcpyToSymbol(c_exp2_64)");
+  }
   g_tables_ready[dev] = true;
   return FABF_OK;
 }
@@ -213,6 +235,14 @@ constexpr int kBSegH = FABF_BSEGH;  // pass-H segment length (columns)
 __device__ __forceinline__ float2 mm2(float2 a, float2 b) {
   return make_float2(fminf(a.x, b.x), fmaxf(a.y, b.y));
 }
+
+// Programmatic dependent launch (PDL): a kernel of the path lets the next one
+// be scheduled as soon as all of its CTAs are running (launch_dependents), and
+// the next one waits for the previous grid's completion and memory flush
+// before touching anything it produced (wait; a no-op when launched without
+// the attribute).  Hides the launch gap and the previous kernel's tail.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Loads are issued kU at a time ahead of the comparison chain (the walk is
 // otherwise one dependent load per sample).
@@ -318,6 +348,42 @@ __device__ __forceinline__ void vhgw_run(const TIn* __restrict__ in, float2* __r
   }
 }
 
+// A full segment of SEG <= w outputs (inputs in[0 .. SEG + w - 2]): every
+// window [o, o + w - 1] is the suffix of block 0 (inputs [0, w)) from o joined
+// with the prefix of block 1 up to o + w - 1, so the suffix values of the SEG
+// output positions stay in registers (compile-time indices) and each output
+// is stored once -- no read-back of the output slot.
+template <int SEG, class TIn, int sin, int sout>
+__device__ __forceinline__ void vhgw_seg(const TIn* __restrict__ in, float2* __restrict__ out, int w) {
+  float2 suf[SEG];
+  float2 run = make_float2(CUDART_INF_F, -CUDART_INF_F);
+  {
+    constexpr int B4 = 4;
+    int i = w - 1;
+    for (; i - (B4 - 1) >= SEG; i -= B4) {  // inputs above the outputs: accumulate only
+      TIn v[B4];
+#pragma unroll
+      for (int u = 0; u < B4; ++u) v[u] = in[(i - u) * sin];
+#pragma unroll
+      for (int u = 0; u < B4; ++u) run = mm2(run, mm_in(v[u]));
+    }
+    for (; i >= SEG; --i) run = mm2(run, mm_in(in[i * sin]));
+  }
+#pragma unroll
+  for (int i = SEG - 1; i >= 0; --i) {
+    run = mm2(run, mm_in(in[i * sin]));
+    suf[i] = run;
+  }
+  out[0] = suf[0];  // o = 0: the window is block 0 itself
+  const TIn* nx = in + (w - 1) * sin;
+  float2 g = make_float2(CUDART_INF_F, -CUDART_INF_F);
+#pragma unroll
+  for (int o = 1; o < SEG; ++o) {
+    g = mm2(g, mm_in(nx[o * sin]));
+    out[o * sout] = mm2(suf[o], g);
+  }
+}
+
 // TMA (cp.async.bulk.tensor) staging of an interior footprint: one thread
 // issues the 3-D box load, the CTA waits on an mbarrier.
 __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, int x, int y, int b,
@@ -379,6 +445,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
                                                       const __grid_constant__ CUtensorMap tmap,
                                                       int use_tma) {
   using G = BoundsGeom<RC>;
+  pdl_trigger();
   __shared__ __align__(8) unsigned long long tbar;
   constexpr int FP = G::FP, VP = G::VP, OP = G::OP;
   extern __shared__ __align__(1024) unsigned char smb[];
@@ -439,7 +506,10 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
     const int c = t % C, s = t / C;
     const int o0 = s * kBSegV, len = min(kBSegV, ny - o0);
     if (kStage) {
-      vhgw_run<float, FP, VP>(F + o0 * FP + c, Vm + o0 * VP + c, len, w);
+      if (len == kBSegV && w >= kBSegV)
+        vhgw_seg<kBSegV, float, FP, VP>(F + o0 * FP + c, Vm + o0 * VP + c, w);
+      else
+        vhgw_run<float, FP, VP>(F + o0 * FP + c, Vm + o0 * VP + c, len, w);
     } else {
       const float* col = src + reflect_index(x0 - rho + c, W);
       const int yb = y0 - rho + o0;
@@ -458,7 +528,10 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
   for (int t = tid; t < ny * segH; t += kThreads) {
     const int r = t % ny, s = t / ny;
     const int o0 = s * kBSegH, len = min(kBSegH, nx - o0);
-    vhgw_run<float2, 1, 1>(Vm + r * VP + o0, O + r * OP + o0, len, w);
+    if (len == kBSegH && w >= kBSegH)
+      vhgw_seg<kBSegH, float2, 1, 1>(Vm + r * VP + o0, O + r * OP + o0, w);
+    else
+      vhgw_run<float2, 1, 1>(Vm + r * VP + o0, O + r * OP + o0, len, w);
   }
   __syncthreads();
   // copy out (coalesced) + the tile's (min alpha, max beta)
@@ -512,6 +585,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
 //      goes to a shared-memory queue, regime-A from the front, B/C from the back;
 //   C2 thread j finishes queue record j (integrals, ratio, guard, store).
 constexpr int kSL = 16;  // lanes per prefix scan
+
 
 // FABF_EXP_TIMERS (experiments only): thread 0 of every CTA accumulates clock64
 // deltas per phase; fabf_exp_timers() reads them back
@@ -616,6 +690,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int cnt[2];  // per step parity: regime-A count (low 16 bits), B/C count (high 16)
   __shared__ float red_min[kThreads / 32], red_max[kThreads / 32];
+  __shared__ double s_etab[64];  // 2^(j/64) for exp_nonpos_tab (C2)
   using G = FilterGeom<N, E>;
   constexpr int NN = G::NN, PSQ = G::PSQ, VST = G::VST;
   constexpr int QS = PPT * kThreads;  // pixels (queue records) per step
@@ -635,10 +710,13 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   float2* VY = reinterpret_cast<float2*>(smraw + lay.vy);    // [RB][YP]
   float2* VZ = reinterpret_cast<float2*>(smraw + lay.vz);    // [RB][YP]
   const float n = (float)(w * w);
-  const bool want_t2n = a.d_t2n != nullptr;
+  const bool want_t2n = a.d_t2n != nullptr, want_kappa = a.d_kappa != nullptr;
   const float2 kEmpty = make_float2(CUDART_INF_F, -CUDART_INF_F);
 
   for (int i = tid; i < RB * NN * PSQ; i += kThreads) Ps[i] = 0.0;  // P[0] = 0 for good
+  if (tid < 64) s_etab[tid] = c_exp2_64[tid];  // read after the first centring barrier
+  pdl_trigger();
+  pdl_wait();  // k_bounds' planes and tile ranges (PDL launch)
 #ifdef FABF_EXP_TIMERS
   unsigned long long t_acc[8] = {};
   long long t_last = clock64();
@@ -859,6 +937,17 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
     // phase-A input prefetch: entering / leaving samples of the next step's rows
     float pf_in[RB], pf_out[RB];
     auto prefetch = [&](int Yb) {
+      const int y0 = Yb + rho;  // entering row of r = 0
+      if (y0 + RB <= H && y0 - w >= 0) {  // (uniform) no reflection: one base, fixed row strides
+        const float* pin = colp + y0 * W;
+        const float* pout = pin - w * W;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          pf_in[r] = __ldg(pin + r * W);
+          pf_out[r] = __ldg(pout + r * W);
+        }
+        return;
+      }
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         const int yin = min(Yb + r + rho, H - 1 + rho), yout = yin - w;
@@ -1205,7 +1294,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               float lam, t0;
               regime = range_params(al, be, th, sg, lam, t0);
             }
-            PixelResult res = ghat_from_record<N>(nu, QS, th, sg, al, be, regime, a.flags, want_t2n, n);
+            PixelResult res = ghat_from_record<N, true>(nu, QS, th, sg, al, be, regime, a.flags, want_t2n, n, s_etab,
+                                                                want_kappa);
             a.out[o] = res.g;
             if (a.d_kappa) a.d_kappa[o] = res.kappa;
             if (a.d_t2n) a.d_t2n[o] = res.t2n;
@@ -1295,6 +1385,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_fallback_seg(FilterArgs a) {
   const int rho = a.rho, w = 2 * rho + 1, H = a.H, W = a.W, Lc = 32 + 2 * rho;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* Vw = reinterpret_cast<double*>(smf) + (size_t)wib * NN * Lc;  // [NN][Lc] this warp's column sums
+  pdl_wait();  // k_filter's segment list (PDL launch)
   const int count = *a.seg_count;
   const int nwarps = gridDim.x * kSegWarps;
   for (int si = blockIdx.x * kSegWarps + wib; si < count; si += nwarps) {
@@ -1905,9 +1996,8 @@ fabf_status_t launch_filter_fb(FilterArgs& fa, cudaStream_t st) {
   if (FB) grid_ll = std::min<long long>(grid_ll, fa.ring_ctas);  // one bounds ring per CTA
   const int grid = (int)grid_ll;
   lk.unlock();
-  k_filter<N, E, TW, PPT, WD, FB><<<grid, kThreads, smem, st>>>(fa);
+  FABF_CUDA(launch_pdl(k_filter<N, E, TW, PPT, WD, FB>, grid, kThreads, smem, st, fa), "k_filter launch");
   ++g_launches;
-  FABF_CUDA(cudaGetLastError(), "k_filter launch");
   return FABF_OK;
 }
 
@@ -1957,9 +2047,8 @@ fabf_status_t launch_filter_n(FilterArgs& fa, int B, cudaStream_t st) {
         attr_set[dev] = true;
       }
     }
-    k_fallback_seg<N><<<148 * 4, 32 * kSegWarps, smem, st>>>(fa);
+    FABF_CUDA(launch_pdl(k_fallback_seg<N>, 148 * 4, 32 * kSegWarps, smem, st, fa), "k_fallback_seg launch");
     ++g_launches;
-    FABF_CUDA(cudaGetLastError(), "k_fallback_seg launch");
   }
   prof_mark(4, st);
   return FABF_OK;

@@ -81,6 +81,26 @@ __device__ __forceinline__ double exp_nonpos(double z) {
   return (z < -708.0) ? 0.0 : p * scale;
 }
 
+// The same with a 64-entry table T[j] = 2^(j/64) (correctly rounded, host
+// computed, staged in shared memory by the caller): K = rint(z 64/ln2),
+// z = K ln2/64 + r with |r| <= ln2/128, exp(z) = 2^(K>>6) T[K&63] exp(r) and a
+// degree-5 Taylor polynomial for exp(r) (truncation r^6/720 < 4e-17): 5 DFMA
+// instead of 12 for one LDS.  z is clamped at -708 (the result is then
+// ~e^-708, not 0: every use here scales a term that is negligible there).
+__constant__ double c_exp2_64[64];
+__device__ __forceinline__ double exp_nonpos_tab(double z, const double* __restrict__ tab) {
+  const double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  const double zc = fmax(z, -708.0);
+  const double ks = fma(zc, 92.33248261689366, kShift);
+  const double kd = ks - kShift;
+  double r = fma(kd, -0.01083042469326756, zc);  // ln2/64, 32 significant bits: kd * hi exact
+  r = fma(kd, -2.9815858269852933e-12, r);
+  const double p = poly_horner<5>(c_exp_poly, r);
+  const int K = __double2loint(ks);
+  const double scale = __hiloint2double(((K >> 6) + 1023) << 20, 0);
+  return (p * tab[K & 63]) * scale;
+}
+
 #include "fabf_erfcx.cuh"
 
 struct PixelResult {
@@ -122,25 +142,32 @@ __constant__ double c_rec[2 * (kMaxN + 1)] = {
     -5.0 / 6, 13.0 / 7, -6.0 / 7, 15.0 / 8, -7.0 / 8, 17.0 / 9, -8.0 / 9, 19.0 / 10, -9.0 / 10,
     21.0 / 11, -10.0 / 11};
 
-template <int N>
+template <int N, bool TAB = false>
 __device__ __forceinline__ void integrals_regime_a(double sk, double s0, double csk, double inv2k,
                                                    const double* nup, int ns, double nu0, double& T2,
-                                                   double& U, double& ab, double& A0, double& X0) {
+                                                   double& U, double& ab, double& A0, double& X0,
+                                                   const double* etab = nullptr) {
   const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);  // s = +1 and s = -1 ends
-  const double qa = xa * xa, qb = xb * xb;
-  const bool a_near = qa < qb;
-  const double qn = a_near ? qa : qb, qf = a_near ? qb : qa;
-  const double E = exp_nonpos(qn - qf);        // <= 1
-  const bool inside = (xa >= 0.0) && (xb >= 0.0);
-  const double Gn = exp_nonpos(inside ? -qn : 0.0);  // scale 1 inside, exp(qn) outside
-  double ca, cb;
-  erfcx_pos2(fabs(xa), fabs(xb), ca, cb);
-  const double cn = a_near ? ca : cb, cf = a_near ? cb : ca;
+  // near / far end first (xa + xb = 2 sk > 0: the far end is never negative)
+  const bool a_near = fabs(xa) < fabs(xb);
+  const double xn = a_near ? xa : xb, xf = a_near ? xb : xa;
+  const double qn = xn * xn, qf = xf * xf;
+  const bool inside = xn >= 0.0;
+  double E, Gn;
+  if constexpr (TAB) {
+    E = exp_nonpos_tab(qn - qf, etab);               // <= 1
+    Gn = exp_nonpos_tab(inside ? -qn : 0.0, etab);   // scale 1 inside, exp(qn) outside
+  } else {
+    E = exp_nonpos(qn - qf);
+    Gn = exp_nonpos(inside ? -qn : 0.0);
+  }
+  double cn, cf;
+  erfcx_pos2(fabs(xn), xf, cn, cf);
   const double gn = Gn, gf = Gn * E;
   // erf(xa) + erf(xb): inside 2 - erfc(xa) - erfc(xb); outside erfc(|x_near|) - erfc(x_far)
   const double a0 = csk * (inside ? (2.0 - cn * gn - cf * gf) : fma(cn, gn, -cf * gf));
-  const double gp = a_near ? gn : gf, gm = a_near ? gf : gn;
-  const double bnd_even = (gp - gm) * inv2k, bnd_odd = (gp + gm) * inv2k;
+  // boundary values g(+1) - g(-1) = +-(gn - gf) (+ when the s = +1 end is the near one)
+  const double bnd_even = (gn - gf) * (a_near ? inv2k : -inv2k), bnd_odd = (gn + gf) * inv2k;
   double a_prev = 0.0, a_cur = a0, d_even = 0.0, d_odd = 0.0;
   // a8 sums consumed on the fly (no A / X arrays): T2 = sum nup_k A_k,
   // U = sum nup_k X_k, ab = sum |nup_k A_k|
@@ -282,11 +309,12 @@ __device__ __forceinline__ void contract(const double* nup, int ns, double nu0, 
   T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A[0], X0f = (float)X[0];
 }
 
-template <int N>
+template <int N, bool TAB = false>
 __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int ns, float theta,
                                                         float sigma, float alpha, float beta,
                                                         int regime, unsigned flags, bool want_t2n,
-                                                        double n) {
+                                                        double n, const double* etab = nullptr,
+                                                        bool want_kappa = true) {
   PixelResult res;
   res.code = 0u;
   double scale_log = 0.0;  // log of the common factor applied to A (diagnostics only)
@@ -318,7 +346,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     const double csk = 2.50662827463100050242 * sg * rd;         // sqrt(pi)/2 / sk
     const double sr = sg * rd, inv2k = 4.0 * sr * sr;             // 1/(2 kappa)
     double T2, U, ab, A0, X0;
-    integrals_regime_a<N>(sk, s0, csk, inv2k, nup, ns, n, T2, U, ab, A0, X0);
+    integrals_regime_a<N, TAB>(sk, s0, csk, inv2k, nup, ns, n, T2, U, ab, A0, X0, etab);
     T2f = (float)T2, Uf = (float)U, abf = (float)ab, A0f = (float)A0, X0f = (float)X0;
     if (want_t2n) {
       const double xa = sk * (1.0 - s0), xb = sk * (1.0 + s0);
@@ -342,7 +370,7 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
   } else {
     ratio = __fdividef(Uf, T2f);  // (2 ulp: the sums carry the cancellation, not the ratio)
   }
-  res.kappa = (T2f > 0.0f) ? abf / T2f : CUDART_INF_F;
+  res.kappa = !want_kappa ? 0.0f : (T2f > 0.0f) ? abf / T2f : CUDART_INF_F;
   // T2 / n in the units of eq.(29) (J = A/2, unscaled)
   res.t2n = want_t2n ? (float)(0.5 * (double)T2f / n * exp(-scale_log)) : 0.0f;
   const float mid = 0.5f * (alpha + beta), half = 0.5f * (beta - alpha);
