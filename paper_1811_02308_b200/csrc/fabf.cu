@@ -39,6 +39,7 @@ struct fabf_plan_s {
   float* alpha = nullptr;  // workspace: bounds
   float* beta = nullptr;
   float2* blkmm = nullptr;  // per bounds tile (min alpha, max beta), fabf_bounds only
+  float2* hmm = nullptr;    // row-pass (min, max) plane of the separable bounds
   // k_filter's vertical-bounds suffix rings (per resident CTA, sized at plan
   // time for the largest rho the shape allows; L2-resident while in use)
   float2* ring = nullptr;
@@ -82,8 +83,12 @@ constexpr int kMaxBands = fabf_plan_s::kMaxBandsPlan;  // fabf_filter_host row b
 constexpr int kFuseRho = 5;
 constexpr long long kFusePixels = 1LL << 21;
 int g_fuse_rho = getenv("FABF_FUSE_RHO") ? atoi(getenv("FABF_FUSE_RHO")) : kFuseRho;
-// segment cap: max(g_seg_min, 3 w) rows (A/B switch FABF_SEG_MIN)
-int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 256;
+// segment cap: max(g_seg_min, g_seg_w w) rows (A/B switch FABF_SEG_MIN)
+int g_seg_min = getenv("FABF_SEG_MIN") ? std::max(8, atoi(getenv("FABF_SEG_MIN"))) : 64;
+// ... and g_seg_w window heights (FABF_SEG_W): long segments save prologues
+// where they are dear (2 rho rows each), short ones keep the centring local
+// (fewer fallback pixels) where they are cheap
+int g_seg_w = getenv("FABF_SEG_W") ? std::max(1, atoi(getenv("FABF_SEG_W"))) : 6;
 // fabf_filter_host row bands per frame (A/B switch FABF_HOST_BANDS, 1..16)
 int g_host_bands = getenv("FABF_HOST_BANDS") ? std::max(1, std::min(16, atoi(getenv("FABF_HOST_BANDS")))) : 6;
 #ifndef FABF_FILTER_MINB
@@ -560,6 +565,164 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const float* __restrict__ i
 }
 
 // ============================================================================
+// step a1, separable in two streaming passes (default): eq.(8) as a row pass
+// and a column pass of the van Herk / Gil-Werman MAX-FILTER (Prop.1,
+// P:266-270; min and max are separable over the box, reflection is per axis):
+//   k_bounds_h: Hmm(y, x) = (min, max) of f(y, x - rho .. x + rho)  (float2 plane)
+//   k_bounds_v: alpha, beta(y, x) = (min, max) of Hmm(y - rho .. y + rho, x),
+//               plus the (min alpha, max beta) of each kBT x kBT tile.
+// Every output segment of SEG <= w positions is one van Herk block boundary
+// (vhgw_regs: suffix in registers, compile-time indices), so each pass reads
+// (SEG + w - 1) / SEG inputs and makes 3 comparisons per output whatever rho
+// is; the whole pass streams: 4 + 8 B/px (h) and 8 + 8 B/px (v) of DRAM, the
+// intermediate plane mostly L2-resident between the two.  Windows narrower
+// than 8 (rho < 4) take direct minima (at most 7 inputs per output).
+template <int SEG, class LoadF>
+__device__ __forceinline__ void vhgw_regs(LoadF in, int w, float2 (&res)[SEG]) {
+  float2 run = make_float2(CUDART_INF_F, -CUDART_INF_F);
+  int i = w - 1;
+  for (; i - 3 >= SEG; i -= 4) {  // inputs above the outputs: accumulate only
+    const float2 v0 = in(i), v1 = in(i - 1), v2 = in(i - 2), v3 = in(i - 3);
+    run = mm2(mm2(run, v0), mm2(mm2(v1, v2), v3));
+  }
+  for (; i >= SEG; --i) run = mm2(run, in(i));
+#pragma unroll
+  for (int j = SEG - 1; j >= 0; --j) {
+    run = mm2(run, in(j));
+    res[j] = run;  // suffix of block 0 from j
+  }
+  float2 g = make_float2(CUDART_INF_F, -CUDART_INF_F);
+#pragma unroll
+  for (int o = 1; o < SEG; ++o) {  // prefix of block 1 up to o + w - 1
+    g = mm2(g, in(o + w - 1));
+    res[o] = mm2(res[o], g);
+  }
+}
+template <int SEG, class LoadF>
+__device__ __forceinline__ void direct_regs(LoadF in, int w, float2 (&res)[SEG]) {
+#pragma unroll
+  for (int o = 0; o < SEG; ++o) {
+    float2 m = in(o);
+    for (int d = 1; d < w; ++d) m = mm2(m, in(o + d));
+    res[o] = m;
+  }
+}
+
+constexpr int kHR = 32;   // k_bounds_h: rows per CTA
+constexpr int kHW = 256;  // k_bounds_h: output columns per CTA
+__host__ __device__ inline int hpass_pitch(int rho) { return (kHW + 2 * rho) | 1; }
+__host__ inline size_t hpass_smem(int rho) {
+  const size_t f = sizeof(float) * (size_t)kHR * hpass_pitch(rho);
+  const size_t o = sizeof(float2) * (size_t)kHR * (kHW + 1);
+  return f > o ? f : o;
+}
+
+// rows [ry0, ry1) of images [b0, b0 + gridDim.z); threads: lane = row of the
+// CTA's 32 (odd pitch: conflict-free), warp = segment group
+template <int SEG, bool DIRECT>
+__global__ void __launch_bounds__(kThreads) k_bounds_h(const float* __restrict__ img, int H, int W, int rho,
+                                                      float2* __restrict__ hmm, int b0, int ry0, int ry1) {
+  extern __shared__ __align__(16) unsigned char smh[];
+  float* F = reinterpret_cast<float*>(smh);    // [kHR][FP] footprint rows
+  float2* O = reinterpret_cast<float2*>(smh);  // [kHR][kHW + 1] results (after the walk)
+  constexpr int NSEG = kHW / SEG, WPT = kHR * NSEG / kThreads;  // walkers per thread
+  const int w = 2 * rho + 1, FP = hpass_pitch(rho);
+  const int x0 = blockIdx.x * kHW, y0 = ry0 + blockIdx.y * kHR, bimg = b0 + blockIdx.z;
+  const int nx = min(kHW, W - x0), ny = min(kHR, ry1 - y0), C = nx + 2 * rho;
+  const size_t plane = (size_t)bimg * H * W;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();
+  // stage the footprint rows (coalesced, reflected at the left / right edges):
+  // cp.async, every element in flight at once, no register round trip
+  const bool inner = x0 - rho >= 0 && x0 + nx + rho <= W;
+  const unsigned fbase = (unsigned)__cvta_generic_to_shared(F);
+  for (int r = warp; r < ny; r += kThreads / 32) {
+    const float* row = img + plane + (size_t)(y0 + r) * W;
+    for (int c = lane; c < C; c += 32) {
+      const float* src = row + (inner ? x0 - rho + c : reflect_index(x0 - rho + c, W));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(fbase + 4u * (unsigned)(r * FP + c)),
+                   "l"(src)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  float2 res[WPT][SEG];
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) {
+    const int s = warp + k * (kThreads / 32);  // segment of row `lane`
+    const float* in = F + lane * FP + s * SEG;
+    auto ld = [&](int i) { const float v = in[i]; return make_float2(v, v); };
+    if (DIRECT)
+      direct_regs<SEG>(ld, w, res[k]);
+    else
+      vhgw_regs<SEG>(ld, w, res[k]);
+  }
+  __syncthreads();  // the footprint is dead: O aliases it
+#pragma unroll
+  for (int k = 0; k < WPT; ++k) {
+    const int s = warp + k * (kThreads / 32);
+#pragma unroll
+    for (int o = 0; o < SEG; ++o) O[lane * (kHW + 1) + s * SEG + o] = res[k][o];
+  }
+  __syncthreads();
+  for (int t = tid; t < ny * kHW; t += kThreads) {
+    const int r = t / kHW, x = t - r * kHW;
+    if (x < nx) hmm[plane + (size_t)(y0 + r) * W + x0 + x] = O[r * (kHW + 1) + x];
+  }
+}
+
+// one CTA per kBT x kBT tile (tile row ty0 + blockIdx.y), kBT * kBT / SEG
+// threads: column tid % kBT (coalesced), segment tid / kBT
+template <int SEG, bool DIRECT>
+__global__ void __launch_bounds__(kBT * kBT / SEG) k_bounds_v(const float2* __restrict__ hmm, int H, int W, int rho,
+                                                             float* __restrict__ amin, float* __restrict__ bmax,
+                                                             float2* __restrict__ blkmm, int b0, int ty0) {
+  constexpr int NT = kBT * kBT / SEG;
+  __shared__ float2 red[NT / 32];
+  const int w = 2 * rho + 1;
+  const int ty = ty0 + blockIdx.y, bimg = b0 + blockIdx.z;
+  const int x0 = blockIdx.x * kBT, y0 = ty * kBT;
+  const int tid = threadIdx.x, c = tid % kBT, s = tid / kBT;
+  const int x = x0 + c, ys = y0 + s * SEG;  // first output row of this thread
+  const size_t plane = (size_t)bimg * H * W;
+  pdl_trigger();
+  pdl_wait();  // k_bounds_h's plane
+  float2 bm = make_float2(CUDART_INF_F, -CUDART_INF_F);
+  if (x < W && ys < H) {
+    const float2* col = hmm + plane + x;
+    float2 res[SEG];
+    if (ys - rho >= 0 && ys + SEG - 1 + rho <= H - 1) {  // no reflection: fixed row stride
+      const float2* base = col + (size_t)(ys - rho) * W;
+      auto ld = [&](int i) { return base[(size_t)i * W]; };
+      if (DIRECT) direct_regs<SEG>(ld, w, res); else vhgw_regs<SEG>(ld, w, res);
+    } else {
+      auto ld = [&](int i) { return col[(size_t)reflect_index(min(ys - rho + i, H - 1 + rho), H) * W]; };
+      if (DIRECT) direct_regs<SEG>(ld, w, res); else vhgw_regs<SEG>(ld, w, res);
+    }
+#pragma unroll
+    for (int o = 0; o < SEG; ++o) {
+      if (ys + o < H) {
+        const size_t off = plane + (size_t)(ys + o) * W + x;
+        amin[off] = res[o].x;
+        bmax[off] = res[o].y;
+        bm = mm2(bm, res[o]);
+      }
+    }
+  }
+  if (blkmm) {
+    for (int off = 16; off > 0; off >>= 1)
+      bm = mm2(bm, make_float2(__shfl_xor_sync(0xffffffffu, bm.x, off), __shfl_xor_sync(0xffffffffu, bm.y, off)));
+    if ((tid & 31) == 0) red[tid >> 5] = bm;
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 1; i < NT / 32; ++i) bm = mm2(bm, red[i]);
+      blkmm[((size_t)bimg * ((H + kBT - 1) / kBT) + ty) * gridDim.x + blockIdx.x] = bm;
+    }
+  }
+}
+
+// ============================================================================
 // steps a1-a8 in one pass (north_star (e)).  Persistent grid,
 // 256 threads; a CTA walks down vertical segments of strips of TW output
 // columns, RB = QS/TW output rows per step.  Per step:
@@ -711,6 +874,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   float2* VZ = reinterpret_cast<float2*>(smraw + lay.vz);    // [RB][YP]
   const float n = (float)(w * w);
   const bool want_t2n = a.d_t2n != nullptr, want_kappa = a.d_kappa != nullptr;
+  const bool want_diag = want_t2n || want_kappa || a.d_code != nullptr;  // fabf_filter_diag
   const float2 kEmpty = make_float2(CUDART_INF_F, -CUDART_INF_F);
 
   for (int i = tid; i < RB * NN * PSQ; i += kThreads) Ps[i] = 0.0;  // P[0] = 0 for good
@@ -1297,9 +1461,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             PixelResult res = ghat_from_record<N, true>(nu, QS, th, sg, al, be, regime, a.flags, want_t2n, n, s_etab,
                                                                 want_kappa);
             a.out[o] = res.g;
-            if (a.d_kappa) a.d_kappa[o] = res.kappa;
-            if (a.d_t2n) a.d_t2n[o] = res.t2n;
-            if (a.d_code) a.d_code[o] = (unsigned char)res.code;
+            if (want_diag) {
+              if (a.d_kappa) a.d_kappa[o] = res.kappa;
+              if (a.d_t2n) a.d_t2n[o] = res.t2n;
+              if (a.d_code) a.d_code[o] = (unsigned char)res.code;
+            }
           }
         }
       }
@@ -1925,11 +2091,71 @@ fabf_status_t launch_bounds_rc(Plan* p, const float* img, int rho, float* alpha,
   return FABF_OK;
 }
 
+// the separable two-pass bounds (k_bounds_h + k_bounds_v) for rows
+// [64 ty0, 64 ty1) of images [b0, b0 + nb)
+template <int SEG, bool DIRECT>
+fabf_status_t launch_bounds_sep_seg(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0,
+                                    int nb, int ty0, int ty1, cudaStream_t st) {
+  const int r0 = ty0 * kBT, r1 = std::min(p->H, ty1 * kBT);
+  const int h0 = std::max(0, r0 - rho), h1 = std::min(p->H, r1 + rho);  // rows the column pass reads
+  const size_t smem = hpass_smem(rho);
+  {
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[p->device]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_bounds_h<SEG, DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMaxDynSmem),
+                "cudaFuncSetAttribute(k_bounds_h)");
+      attr_set[p->device] = true;
+    }
+  }
+  dim3 gh((p->W + kHW - 1) / kHW, (h1 - h0 + kHR - 1) / kHR, nb);
+  k_bounds_h<SEG, DIRECT><<<gh, kThreads, smem, st>>>(img, p->H, p->W, rho, p->hmm, b0, h0, h1);
+  ++g_launches;
+  FABF_CUDA(cudaGetLastError(), "k_bounds_h launch");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((p->W + kBT - 1) / kBT, ty1 - ty0, nb);
+  cfg.blockDim = dim3(kBT * kBT / SEG);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  FABF_CUDA(cudaLaunchKernelEx(&cfg, k_bounds_v<SEG, DIRECT>, (const float2*)p->hmm, p->H, p->W, rho, alpha, beta,
+                               p->blkmm, b0, ty0),
+            "k_bounds_v launch");
+  ++g_launches;
+  return FABF_OK;
+}
+fabf_status_t launch_bounds_sep(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0, int nb,
+                                int ty0, int ty1, cudaStream_t st) {
+  const int w = 2 * rho + 1;
+  if (w >= 32) return launch_bounds_sep_seg<32, false>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+  if (w >= 16) return launch_bounds_sep_seg<16, false>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+  if (w >= 8) return launch_bounds_sep_seg<8, false>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+  return launch_bounds_sep_seg<8, true>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+}
+
+// bounds placement: the separable passes (default) or the 2-D tile kernel
+// k_bounds (FABF_BOUNDS=tile: A/B switch)
+// (default: tile kernel for rho <= 24, where two of its CTAs fit an SM;
+// separable passes above; FABF_BOUNDS=tile / sep forces one)
+int g_bounds_mode = !getenv("FABF_BOUNDS") ? 0 : std::string(getenv("FABF_BOUNDS")) == "tile" ? 1
+                    : std::string(getenv("FABF_BOUNDS")) == "sep" ? 2 : 0;
+
 // rows [64 ty0, 64 ty1) of images [b0, b0 + nb)
 fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0,
                             int nb, int ty0, int ty1, cudaStream_t st) {
   prof_mark(0, st);
   fabf_status_t s;
+  if (g_bounds_mode == 2 || (g_bounds_mode == 0 && rho > 24)) {
+    s = launch_bounds_sep(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+    if (s != FABF_OK) return s;
+    prof_mark(1, st);
+    prof_mark(2, st);
+    return FABF_OK;
+  }
   if (rho <= 8)
     s = launch_bounds_rc<8>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
   else if (rho <= 24)
@@ -2170,7 +2396,7 @@ fabf_status_t filter_band(Plan* p, const float* img, const float* theta, const f
   fa.r0 = ty0 * kBT;
   fa.r1 = std::min(p->H, ty1 * kBT);
   // segment cap (rows): fresh fp64 sums every few window heights
-  fa.SH = std::max(g_seg_min, 3 * (2 * rho + 1));
+  fa.SH = std::max(g_seg_min, g_seg_w * (2 * rho + 1));
   fa.flags = p->flags;
   fa.ring = p->ring;
   fa.ring_cta = ring_elems_per_cta(rho);
@@ -2327,6 +2553,7 @@ fabf_status_t fabf_plan(fabf_plan_t* plan, int batch, int height, int width, uns
   cudaError_t e;
   if ((e = cudaMalloc(&p->alpha, px * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&p->beta, px * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&p->hmm, px * sizeof(float2))) != cudaSuccess ||
       (e = cudaMalloc(&p->blkmm, sizeof(float2) * (size_t)batch * ((height + kBT - 1) / kBT) *
                                      ((width + kBT - 1) / kBT))) != cudaSuccess ||
       (e = cudaMalloc(&p->fb_count, sizeof(int) * (size_t)batch * Plan::kMaxBandsPlan)) != cudaSuccess ||
@@ -2750,6 +2977,7 @@ fabf_status_t fabf_destroy(fabf_plan_t plan) {
   if (!p) return FABF_OK;
   cudaFree(p->alpha);
   cudaFree(p->beta);
+  cudaFree(p->hmm);
   cudaFree(p->blkmm);
   cudaFree(p->ring);
   cudaFree(p->fb_count);

@@ -23,6 +23,10 @@ for k in k_filter k_bounds; do
   ncu -i $R --page source --csv --print-source cuda,sass 2> /dev/null | gzip -9 > gpurun_out/source_${k}_$TAG.csv.gz
   python tools/ncu_ops.py $R > gpurun_out/ops_${k}_$TAG.txt 2>&1
 done
+if [ -n "$SWEEP" ]; then
+  timeout 1500 python bench.py --sweep --steps 5 --warmup 2 > gpurun_out/sweep_$TAG.jsonl 2>&1
+  echo "sweep rc $?" >> gpurun_out/sweep_$TAG.jsonl
+fi
 cp profiles/traffic.json gpurun_out/traffic_before_$TAG.json
 python tools/ncu_traffic.py k_filter=gpurun_out/prof_k_filter_$TAG.ncu-rep k_bounds=gpurun_out/prof_k_bounds_$TAG.ncu-rep > gpurun_out/traffic_$TAG.log 2>&1
 cp profiles/traffic.json gpurun_out/traffic_$TAG.json

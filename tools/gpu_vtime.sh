@@ -10,7 +10,7 @@ if [ -n "$CHECK" ]; then
 fi
 for rep in 1 2 3; do
   for v in $VARS; do
-    name=${v%%:*}; envs=""; [ "$name" != "$v" ] && envs=${v#*:}
+    name=${v%%:*}; envs=""; [ "$name" != "$v" ] && envs=${v#*:}; envs=${envs//,/ }
     env $envs FABF_LIB=$PWD/vlibs/libfabf_$name.so timeout 300 python tools/time_cfg.py ${CFG:-4} 2>&1 | sed "s/^/$v /" >> gpurun_out/time_$TAG.log
   done
 done
