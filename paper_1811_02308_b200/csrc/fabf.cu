@@ -1569,15 +1569,6 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_fallback_seg(FilterArgs a) {
     const size_t o = (size_t)b * H * W + (size_t)y * W + x;
     float al = 0.f, be = 0.f;
     if (flagged) al = a.alpha_w[o], be = a.beta_w[o];
-    float umin = flagged ? al : CUDART_INF_F, umax = flagged ? be : -CUDART_INF_F;
-    for (int off = 16; off > 0; off >>= 1) {
-      umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, off));
-      umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
-    }
-    const double cT = 0.5 * ((double)umin + (double)umax), halfr = 0.5 * ((double)umax - (double)umin);
-    int e2 = 0;
-    if (halfr > 0.0) frexp(halfr, &e2);
-    const double invS = ldexp(1.0, -e2), mcs = -cT * invS;
     if (rho <= kSegDirectRho) {  // small windows: each lane's direct sums are cheaper than the columns
       if (flagged) {
         const float th = a.theta[o], sg = a.sigma[o];
@@ -1589,54 +1580,140 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_fallback_seg(FilterArgs a) {
       }
       continue;
     }
-    // column power sums over the window rows, lanes over the segment's columns
-    for (int cc = lane; cc < Lc; cc += 32) {
-      const float* col = img + reflect_index(min(x0 - rho + cc, W - 1 + rho), W);
-      double V[NN];
-#pragma unroll
-      for (int q = 0; q < NN; ++q) V[q] = 0.0;
-      for (int dy = -rho; dy <= rho; ++dy) {
-        const double u = fma((double)__ldg(col + reflect_index(y + dy, H) * W), invS, mcs);
-        double pu = u;
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-          V[q] += pu;
-          pu *= u;
+    float th = 0.f, sg = 1.f;
+    if (flagged) th = a.theta[o], sg = a.sigma[o];
+    // The segment's flagged lanes are served in clusters of compatible ranges
+    // (a segment may straddle two flat areas): greedy in lane order from the
+    // lowest pending lane, the union of the members' [alpha, beta] may grow
+    // while its half-range stays within flag_root / 3 of the narrowest
+    // member's (then every member passes the amplification test against the
+    // union's centre and power-of-two scale); one pass of column power sums
+    // per cluster.  A member that still fails (never the first) waits for a
+    // later cluster; the first one failing -- impossible by construction --
+    // would take the exact direct sums.
+    const float lim = (float)(a.flag_root_direct / 3.0);
+    unsigned pending = __ballot_sync(0xffffffffu, flagged);
+    // greedy cluster from the lowest lane of `rem`: members and their union
+    auto greedy = [&](unsigned rem, float& cl, float& ch) {
+      const int r = __ffs(rem) - 1;
+      cl = __shfl_sync(0xffffffffu, al, r), ch = __shfl_sync(0xffffffffu, be, r);
+      float hmin = 0.5f * (ch - cl);
+      unsigned mem = 1u << r;
+      for (int j = r + 1; j < 32; ++j) {  // warp-uniform
+        const float aj = __shfl_sync(0xffffffffu, al, j), bj = __shfl_sync(0xffffffffu, be, j);
+        if (!((rem >> j) & 1u)) continue;
+        const float nl = fminf(cl, aj), nh = fmaxf(ch, bj), nhm = fminf(hmin, 0.5f * (bj - aj));
+        if (0.5f * (nh - nl) <= lim * nhm) cl = nl, ch = nh, hmin = nhm, mem |= 1u << j;
+      }
+      return mem;
+    };
+    bool first = true, counted = false;
+    while (pending) {
+      const int r0 = __ffs(pending) - 1;
+      float cl, ch;
+      unsigned members;
+      if (first) {  // first pass: the union of every flagged lane (one pass serves most segments)
+        float umin = flagged ? al : CUDART_INF_F, umax = flagged ? be : -CUDART_INF_F;
+        for (int off = 16; off > 0; off >>= 1) {
+          umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, off));
+          umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+        }
+        cl = umin, ch = umax, members = pending;
+      } else {  // then greedy clusters of the lanes that failed it
+        members = greedy(pending, cl, ch);
+        if (!counted) {
+          // as many cluster passes as that takes, or every remaining lane's
+          // exact direct window sums in parallel -- whichever is cheaper
+          // (per-lane samples: (32 + 2 rho) w / 32 + w per pass, w^2 direct)
+          counted = true;
+          int k = 0;
+          for (unsigned rem = pending; rem; ++k) {
+            float l2, h2;
+            rem &= ~greedy(rem, l2, h2);
+          }
+          if ((float)k * (float)((32 + 2 * rho) * w / 32 + w) > (float)(w * w)) {
+            if ((pending >> lane) & 1u) {
+              const PixelResult res = fallback_direct<N>(a, img, x, y, al, be, th, sg);
+              a.out[o] = res.g;
+              if (a.d_kappa) a.d_kappa[o] = res.kappa;
+              if (a.d_t2n) a.d_t2n[o] = res.t2n;
+              if (a.d_code) a.d_code[o] = (unsigned char)(res.code | kCodeFallback);
+            }
+            __syncwarp();
+            break;
+          }
         }
       }
+      const double cT = 0.5 * ((double)cl + (double)ch), halfr = 0.5 * ((double)ch - (double)cl);
+      int e2 = 0;
+      if (halfr > 0.0) frexp(halfr, &e2);
+      const double invS = ldexp(1.0, -e2), mcs = -cT * invS;
+      // column power sums over the window rows, lanes over the segment's columns
+      for (int cc = lane; cc < Lc; cc += 32) {
+        const float* col = img + reflect_index(min(x0 - rho + cc, W - 1 + rho), W);
+        double V[NN];
 #pragma unroll
-      for (int q = 0; q < N; ++q) Vw[q * Lc + cc] = V[q];
-    }
-    __syncwarp();
-    if (flagged) {
-      const float th = a.theta[o], sg = a.sigma[o];
-      const double au = fma((double)al, invS, mcs), bu = fma((double)be, invS, mcs);
-      PixelResult res;
-      unsigned code = kCodeFallback;
-      if (stretch_flagged(au, bu, a.flag_root_direct)) {  // still amplified: the exact direct sums
-        res = fallback_direct<N>(a, img, x, y, al, be, th, sg);
-      } else {
-        double S[N + 1];
-        S[0] = (double)(w * w);
+        for (int q = 0; q < NN; ++q) V[q] = 0.0;
+        const bool inside = y - rho >= 0 && y + rho <= H - 1;
+        for (int dy0 = -rho; dy0 <= rho; dy0 += 4) {
+          float fv[4];
 #pragma unroll
-        for (int q = 1; q <= N; ++q) {
-          double acc = 0.0;
-          const double* v = Vw + (q - 1) * Lc + lane;
-          for (int d = 0; d < w; ++d) acc += v[d];
-          S[q] = acc;
+          for (int k = 0; k < 4; ++k) {  // loads ahead of the arithmetic
+            const int yy = y + min(dy0 + k, rho);
+            fv[k] = __ldg(col + (inside ? yy : reflect_index(yy, H)) * W);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (dy0 + k <= rho) {
+              const double u = fma((double)fv[k], invS, mcs);
+              double pu = u;
+#pragma unroll
+              for (int q = 0; q < N; ++q) {
+                V[q] += pu;
+                pu *= u;
+              }
+            }
+          }
         }
-        double nup[NN];
-        nu_from_sums<N>(S, au, bu, nup, 1);
-        float lam, t0;
-        const int regime = range_params(al, be, th, sg, lam, t0);
-        res = ghat_from_record<N>(nup, 1, th, sg, al, be, regime, a.flags, a.d_t2n != nullptr, (double)(w * w));
+#pragma unroll
+        for (int q = 0; q < N; ++q) Vw[q * Lc + cc] = V[q];
       }
-      a.out[o] = res.g;
-      if (a.d_kappa) a.d_kappa[o] = res.kappa;
-      if (a.d_t2n) a.d_t2n[o] = res.t2n;
-      if (a.d_code) a.d_code[o] = (unsigned char)(res.code | code);
+      __syncwarp();
+      bool served = false;
+      if ((members >> lane) & 1u) {
+        const double au = fma((double)al, invS, mcs), bu = fma((double)be, invS, mcs);
+        const bool amplified = stretch_flagged(au, bu, a.flag_root_direct);
+        if (!amplified || (lane == r0 && !first)) {
+          PixelResult res;
+          if (amplified) {
+            res = fallback_direct<N>(a, img, x, y, al, be, th, sg);
+          } else {
+            double S[N + 1];
+            S[0] = (double)(w * w);
+#pragma unroll
+            for (int q = 1; q <= N; ++q) S[q] = 0.0;
+            for (int d = 0; d < w; ++d) {  // N independent chains
+#pragma unroll
+              for (int q = 1; q <= N; ++q) S[q] += Vw[(q - 1) * Lc + lane + d];
+            }
+            double nup[NN];
+            nu_from_sums<N>(S, au, bu, nup, 1);
+            float lam, t0;
+            const int regime = range_params(al, be, th, sg, lam, t0);
+            res = ghat_from_record<N>(nup, 1, th, sg, al, be, regime, a.flags, a.d_t2n != nullptr,
+                                      (double)(w * w));
+          }
+          a.out[o] = res.g;
+          if (a.d_kappa) a.d_kappa[o] = res.kappa;
+          if (a.d_t2n) a.d_t2n[o] = res.t2n;
+          if (a.d_code) a.d_code[o] = (unsigned char)(res.code | kCodeFallback);
+          served = true;
+        }
+      }
+      pending &= ~__ballot_sync(0xffffffffu, served);
+      first = false;
+      __syncwarp();  // Vw reused by the next cluster / segment
     }
-    __syncwarp();  // Vw reused by the warp's next segment
   }
 }
 

@@ -573,3 +573,50 @@ def test_gaussian_spatial_kernel_fallback(fb, orc):
     o = orc.fast(f, th, sg, 2, 10, spatial="gauss")
     mx, nbad, _ = compare_guarded(out.cpu().numpy(), o, 1.0)
     assert nbad == 0, f"max |delta| = {mx} grey"
+
+
+# ------------------------------------------------------------------ A/B switches of the library
+_PLACEMENT_SCRIPT = r"""
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.environ["FABF_ROOT"])
+import paper_1811_02308_b200 as fb
+import workloads
+res = {}
+for shape, rho in [((1, 150, 260), 7), ((2, 130, 300), 20), ((1, 200, 333), 30), ((1, 193, 517), 60)]:
+    rng = np.random.default_rng(sum(shape) + rho)
+    f = rng.normal(100, 60, shape).astype(np.float32)
+    plan = fb.Plan(*shape)
+    a, b = fb.bounds(plan, torch.from_numpy(f).cuda(), rho)
+    res[f"f_{rho}"], res[f"a_{rho}"], res[f"b_{rho}"] = f, a.cpu().numpy(), b.cpu().numpy()
+w = workloads.random_case(1, 160, 300, seed=5, kind="voronoi", rho=30, N=6)
+plan = fb.Plan(*w.shape)
+d = lambda x: torch.from_numpy(x).cuda()
+res["g"] = fb.filter(plan, d(w.img), d(w.theta), d(w.sigma), w.rho, w.N).cpu().numpy()
+np.savez(sys.argv[1], **res)
+"""
+
+
+@pytest.mark.parametrize("env", [{"FABF_BOUNDS": "tile"}, {"FABF_BOUNDS": "sep"}, {"FABF_PDL": "0"}])
+def test_library_switches_bit_identical(fb, orc, tmp_path, env):
+    """The library's A/B switches (read once at load: bounds by the 2-D tile
+    kernel or the separable passes at every rho, programmatic dependent launch
+    off) give the same bit-exact bounds (oracle scan) and the same filter
+    output as the default placement."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, extra in (("default", {}), ("switched", env)):
+        path = str(tmp_path / f"{name}.npz")
+        e = dict(os.environ, FABF_ROOT=root, **extra)
+        subprocess.run([sys.executable, "-c", _PLACEMENT_SCRIPT, path], env=e, check=True, timeout=600)
+        outs[name] = np.load(path)
+    for rho in (7, 20, 30, 60):
+        f = outs["default"][f"f_{rho}"]
+        ra, rb = orc.bounds(f, rho)
+        for name in outs:
+            assert np.array_equal(outs[name][f"a_{rho}"], ra), (name, rho)
+            assert np.array_equal(outs[name][f"b_{rho}"], rb), (name, rho)
+    assert np.array_equal(outs["default"]["g"], outs["switched"]["g"])
