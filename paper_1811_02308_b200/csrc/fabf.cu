@@ -723,6 +723,127 @@ __global__ void __launch_bounds__(kBT * kBT / SEG) k_bounds_v(const float2* __re
 }
 
 // ============================================================================
+// step a1, default for 8 <= rho <= 24 on large images: one CTA per 64-column x
+// 128-row output tile (two kBT x kBT bounds tiles).  The (128 + 2 rho) x
+// (64 + 2 rho) footprint of f is staged with a 512-byte row pitch (cp.async,
+// 16-byte copies for interior tiles); the row pass (van Herk / Gil-Werman,
+// vhgw_regs: suffix in registers) turns each footprint row into its 64
+// horizontal (min, max) pairs IN PLACE (a row of 64 float2 is 512 bytes), and
+// the column pass walks those rows down each column and writes alpha, beta
+// straight to global memory (lane = column: coalesced) with the two tiles'
+// (min alpha, max beta).  Against the 64 x 64 tile kernel: the vertical halo
+// is shared by two tiles (footprint rows 1.31x instead of 1.63x the outputs),
+// the horizontal halo costs loads only, and no output staging.
+constexpr int kB2C = 64, kB2R = 128;  // output columns / rows per CTA
+constexpr int kB2P = 130;             // footprint row pitch (floats): one row of 65 float2, 2-way conflicts at most
+__host__ inline size_t bounds2_smem(int rho) { return sizeof(float) * (size_t)kB2P * (kB2R + 2 * rho); }
+
+template <int SEGH, int SEGV>
+__global__ void __launch_bounds__(kThreads) k_bounds2(const float* __restrict__ img, int H, int W, int rho,
+                                                     float* __restrict__ amin, float* __restrict__ bmax,
+                                                     float2* __restrict__ blkmm, int b0, int ty0, int ty1) {
+  extern __shared__ __align__(16) unsigned char smb2[];
+  __shared__ float2 red[2 * kThreads / 32];
+  float* F = reinterpret_cast<float*>(smb2);    // [FR][kB2P] footprint rows
+  float2* Hm = reinterpret_cast<float2*>(smb2);  // [FR][kB2P / 2] row-pass results, in place
+  const int w = 2 * rho + 1;
+  const int x0 = blockIdx.x * kB2C, y0 = (ty0 + 2 * blockIdx.y) * kBT, bimg = b0 + blockIdx.z;
+  const int yend = min(H, ty1 * kBT);  // rows this launch writes
+  const int ny = min(kB2R, yend - y0), FR = ny + 2 * rho, C = kB2C + 2 * rho;
+  const size_t plane = (size_t)bimg * H * W;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();
+  // ---- stage the footprint (rows y0 - rho .., columns x0 - rho ..), reflected at the borders
+  const unsigned fbase = (unsigned)__cvta_generic_to_shared(F);
+  const bool inner = x0 - rho >= 0 && x0 + kB2C + rho <= W && y0 - rho >= 0 && y0 + ny + rho <= H;
+  int delta = 0;
+  const int xs = (x0 - rho) & ~1, nq = (C + (x0 - rho - xs) + 1) >> 1;  // float2 per row (<= kB2P / 2)
+  if (inner && (W & 1) == 0 && xs + 2 * nq <= W) {  // 8-byte copies from the even column below x0 - rho
+    delta = (x0 - rho) - xs;
+    const float* src = img + plane + (size_t)(y0 - rho + warp) * W + xs + 2 * lane;
+    unsigned dst = fbase + 4u * (unsigned)(warp * kB2P + 2 * lane);
+    for (int r = warp; r < FR; r += kThreads / 32, src += (kThreads / 32) * (size_t)W, dst += 4u * (kThreads / 32) * kB2P) {
+#pragma unroll
+      for (int q = 0; q < kB2P / 2; q += 32)
+        if (q + lane < nq)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * q), "l"(src + 2 * q) : "memory");
+    }
+  } else {
+    for (int r = warp; r < FR; r += kThreads / 32) {
+      const float* row = img + plane + (size_t)reflect_index(min(y0 - rho + r, H - 1 + rho), H) * W;
+      for (int c = lane; c < C; c += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(fbase + 4u * (unsigned)(r * kB2P + c)),
+                     "l"(row + reflect_index(min(x0 - rho + c, W - 1 + rho), W))
+                     : "memory");
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  // ---- row pass, in place, in rounds of kThreads walkers (a round's rows are
+  // read completely before any of them is overwritten)
+  constexpr int NSH = kB2C / SEGH;  // segments per row
+  constexpr int RPR = kThreads / NSH;  // rows per round
+  for (int rr = 0; rr < FR; rr += RPR) {
+    // lane = row (32 consecutive rows per warp, one segment): banks 2 r + c
+    const int s = (tid >> 5) % NSH, r = rr + lane + 32 * ((tid >> 5) / NSH);
+    float2 res[SEGH];
+    const bool act = r < FR;
+    if (act) {
+      const float* in = F + r * kB2P + delta + s * SEGH;
+      vhgw_regs<SEGH>([&](int i) { const float v = in[i]; return make_float2(v, v); }, w, res);
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int o = 0; o < SEGH; ++o) Hm[r * (kB2P / 2) + s * SEGH + o] = res[o];
+    }
+    __syncthreads();
+  }
+  // ---- column pass: lane = column, warp = segment of SEGV output rows
+  constexpr int NSV = kB2R / SEGV;  // segments per column
+  float2 bm[2] = {make_float2(CUDART_INF_F, -CUDART_INF_F), make_float2(CUDART_INF_F, -CUDART_INF_F)};
+  for (int t = tid; t < kB2C * NSV; t += kThreads) {
+    const int c = t % kB2C, s = t / kB2C;
+    const int x = x0 + c, ys = s * SEGV;  // first output row (tile-relative)
+    if (ys < ny) {
+      float2 res[SEGV];
+      const float2* in = Hm + ys * (kB2P / 2) + c;
+      vhgw_regs<SEGV>([&](int i) { return in[i * (kB2P / 2)]; }, w, res);
+      if (x < W) {
+        float2 m = make_float2(CUDART_INF_F, -CUDART_INF_F);
+#pragma unroll
+        for (int o = 0; o < SEGV; ++o) {
+          if (ys + o < ny) {
+            const size_t off = plane + (size_t)(y0 + ys + o) * W + x;
+            amin[off] = res[o].x;
+            bmax[off] = res[o].y;
+            m = mm2(m, res[o]);
+          }
+        }
+        if (ys < kBT) bm[0] = mm2(bm[0], m); else bm[1] = mm2(bm[1], m);  // SEGV divides kBT
+      }
+    }
+  }
+  if (blkmm) {  // the two kBT x kBT tiles' (min alpha, max beta)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      for (int off = 16; off > 0; off >>= 1)
+        bm[h] = mm2(bm[h], make_float2(__shfl_xor_sync(0xffffffffu, bm[h].x, off),
+                                       __shfl_xor_sync(0xffffffffu, bm[h].y, off)));
+    __syncthreads();  // (Hm reads done before red is written: red is separate anyway)
+    if (lane == 0) red[warp] = bm[0], red[kThreads / 32 + warp] = bm[1];
+    __syncthreads();
+    if (tid < 2) {
+      float2 m = make_float2(CUDART_INF_F, -CUDART_INF_F);
+      for (int wi = 0; wi < kThreads / 32; ++wi) m = mm2(m, red[tid * (kThreads / 32) + wi]);
+      const int ty = ty0 + 2 * blockIdx.y + tid;
+      if (ty < ty1 && ty * kBT < H)
+        blkmm[((size_t)bimg * ((H + kBT - 1) / kBT) + ty) * ((W + kBT - 1) / kBT) + blockIdx.x] = m;
+    }
+  }
+}
+
+// ============================================================================
 // steps a1-a8 in one pass (north_star (e)).  Persistent grid,
 // 256 threads; a CTA walks down vertical segments of strips of TW output
 // columns, RB = QS/TW output rows per step.  Per step:
@@ -2216,16 +2337,50 @@ fabf_status_t launch_bounds_sep(Plan* p, const float* img, int rho, float* alpha
 
 // bounds placement: the separable passes (default) or the 2-D tile kernel
 // k_bounds (FABF_BOUNDS=tile: A/B switch)
-// (default: tile kernel for rho <= 24, where two of its CTAs fit an SM;
-// separable passes above; FABF_BOUNDS=tile / sep forces one)
+// (default: the 64 x 128 in-place kernel k_bounds2 for 8 <= rho <= 24, the
+// 64 x 64 tile kernel below, the separable passes above; FABF_BOUNDS=tile /
+// sep / t2 forces one where it applies)
 int g_bounds_mode = !getenv("FABF_BOUNDS") ? 0 : std::string(getenv("FABF_BOUNDS")) == "tile" ? 1
-                    : std::string(getenv("FABF_BOUNDS")) == "sep" ? 2 : 0;
+                    : std::string(getenv("FABF_BOUNDS")) == "sep" ? 2
+                    : std::string(getenv("FABF_BOUNDS")) == "t2" ? 3 : 0;
+
+template <int SEGH, int SEGV>
+fabf_status_t launch_bounds2_seg(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0, int nb,
+                                 int ty0, int ty1, cudaStream_t st) {
+  const size_t smem = bounds2_smem(rho);
+  {
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[p->device]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_bounds2<SEGH, SEGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_bounds2)");
+      attr_set[p->device] = true;
+    }
+  }
+  dim3 g((p->W + kB2C - 1) / kB2C, (ty1 - ty0 + 1) / 2, nb);
+  k_bounds2<SEGH, SEGV><<<g, kThreads, smem, st>>>(img, p->H, p->W, rho, alpha, beta, p->blkmm, b0, ty0, ty1);
+  ++g_launches;
+  FABF_CUDA(cudaGetLastError(), "k_bounds2 launch");
+  return FABF_OK;
+}
+fabf_status_t launch_bounds2(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0, int nb,
+                             int ty0, int ty1, cudaStream_t st) {
+  if (2 * rho + 1 >= 32) return launch_bounds2_seg<32, 32>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+  return launch_bounds2_seg<16, 16>(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+}
 
 // rows [64 ty0, 64 ty1) of images [b0, b0 + nb)
 fabf_status_t launch_bounds(Plan* p, const float* img, int rho, float* alpha, float* beta, int b0,
                             int nb, int ty0, int ty1, cudaStream_t st) {
   prof_mark(0, st);
   fabf_status_t s;
+  if ((g_bounds_mode == 0 || g_bounds_mode == 3) && rho >= 8 && rho <= 24) {
+    s = launch_bounds2(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
+    if (s != FABF_OK) return s;
+    prof_mark(1, st);
+    prof_mark(2, st);
+    return FABF_OK;
+  }
   if (g_bounds_mode == 2 || (g_bounds_mode == 0 && rho > 24)) {
     s = launch_bounds_sep(p, img, rho, alpha, beta, b0, nb, ty0, ty1, st);
     if (s != FABF_OK) return s;
