@@ -254,8 +254,15 @@ def run_gpu(args):
 
     build.build()
     import workloads
+    from paper_1811_02308_b200.shard import frame_shard
 
-    w = workloads.config(CFG)
+    # N > 1: a batch of one config-4 frame per GPU, sharded over the ranks
+    # (frame_shard: rank r owns frame r; frame 0 is the BASELINE frame, the
+    # others are drawn from the same recipe with their own seeds) -- no
+    # data-path collective, each rank filters and keeps its own frame
+    first, count = frame_shard(ws, ws, rank)
+    assert count == 1
+    w = workloads.config(CFG, frame=first)
     B, H, W = w.shape
     px = B * H * W
     img = torch.from_numpy(w.img).to(dev)
@@ -385,7 +392,8 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
             "config": {"workload": w.name, "height": H, "width": W, "rho": w.rho, "N": w.N,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                       "parallelism": f"{ws} independent frames (one per GPU)" if ws > 1 else "1 GPU"},
+                       "parallelism": f"{ws} frames sharded one per GPU (frame_shard), no data-path collective"
+                       if ws > 1 else "1 GPU"},
             "roofline": fp64,
             "hbm_roofline": hbm,
             "step_ms": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms),

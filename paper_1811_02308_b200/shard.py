@@ -19,6 +19,25 @@ def frame_shard(batch: int, world: int, rank: int) -> tuple[int, int]:
     return first, base + (1 if rank < extra else 0)
 
 
+def gather_frames(local, batch: int, world: int, rank: int):
+    """Reassemble a sharded batch on every rank: ``local`` holds this rank's
+    frames (first axis, in frame_shard order, host arrays); returns the whole
+    (batch, ...) array.  The only data-path collective of the sharded path,
+    used when a caller wants the frames back in one place (the bench does not:
+    each rank keeps its own output)."""
+    import numpy as np
+    import torch.distributed as dist
+
+    first, n = frame_shard(batch, world, rank)
+    if len(local) != n:
+        raise ValueError(f"rank {rank} holds {len(local)} frames, its shard has {n}")
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return np.asarray(local)
+    parts = [None] * world
+    dist.all_gather_object(parts, (first, np.asarray(local)))
+    return np.concatenate([p for _, p in sorted(parts, key=lambda t: t[0]) if len(p)], axis=0)
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar (the device time of the timed region) over the
     process group; identity without an initialised group."""

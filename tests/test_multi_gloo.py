@@ -70,3 +70,56 @@ def test_gloo_world2_max_over_ranks():
     res = sorted(q.get(timeout=10) for _ in range(2))
     assert [(r, f, n) for r, f, n, _ in res] == [(0, 0, 16), (1, 16, 16)]
     assert all(t == pytest.approx(2.5) for *_, t in res)  # both ranks see the max
+
+
+def _pipeline_worker(rank, world, port, q):
+    """One rank of the sharded path on CPU: its frames of a small batch,
+    filtered by the oracle (standing in for the device kernels, which need a
+    GPU), gathered back with shard.gather_frames."""
+    import numpy as np
+    import torch.distributed as dist
+
+    import oracle
+    import workloads
+    from paper_1811_02308_b200.shard import frame_shard, gather_frames
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = workloads.random_case(5, 20, 23, seed=11, kind="voronoi", rho=2, N=3)
+        first, n = frame_shard(5, world, rank)
+        sl = slice(first, first + n)
+        local = oracle.fast(w.img[sl], w.theta[sl], w.sigma[sl], w.rho, w.N)["g_guard"] if n else np.empty((0, 20, 23))
+        full = gather_frames(local, 5, world, rank)
+        q.put((rank, n, full))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_pipeline_matches_single_process():
+    """World size 2: each rank filters only its frame shard; the gathered
+    batch equals the single-process result frame for frame (frames are
+    independent problems: no halo, no other collective)."""
+    import numpy as np
+    import torch.multiprocessing as mp
+
+    import oracle
+    import workloads
+
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = sorted((q.get(timeout=10) for _ in range(2)), key=lambda t: t[0])
+    assert [n for _, n, _ in res] == [3, 2]
+    w = workloads.random_case(5, 20, 23, seed=11, kind="voronoi", rho=2, N=3)
+    ref = oracle.fast(w.img, w.theta, w.sigma, w.rho, w.N)["g_guard"]
+    for _, _, full in res:
+        assert np.array_equal(full, ref)

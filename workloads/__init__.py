@@ -114,22 +114,31 @@ def _stack(x):
     return np.ascontiguousarray(x[None] if x.ndim == 2 else x, dtype=np.float32)
 
 
-def config(cfg: int, scale: float = 1.0) -> Workload:
+def config(cfg: int, scale: float = 1.0, frame: int = 0) -> Workload:
     """Configs 1-4 of BASELINE.json (1-based as printed there).
 
-    ``scale`` < 1 shrinks the image (for quick tests) while keeping rho and N."""
+    ``scale`` < 1 shrinks the image (for quick tests) while keeping rho and N.
+    ``frame`` > 0 draws another frame of the same recipe (other seeds; frame 0
+    is the BASELINE frame) -- the frames a multi-GPU run shards over ranks."""
+    if frame:
+        w = _config_seeded(cfg, scale, 1000 * cfg + 10007 * frame)
+        return Workload(f"{w.name}_frame{frame}", w.img, w.theta, w.sigma, w.rho, w.N)
+    return _config_seeded(cfg, scale, 1000 * cfg)
+
+
+def _config_seeded(cfg: int, scale: float, seed: int) -> Workload:
     from scipy import ndimage
 
     if cfg == 1:
         H = W = max(16, int(256 * scale))
-        f = rectangles(H, W, 1000 * cfg)
-        rng = np.random.default_rng(1000 * cfg + 500)
+        f = rectangles(H, W, seed)
+        rng = np.random.default_rng(seed + 500)
         sigma = rng.uniform(10, 40, f.shape)
         theta = f + rng.uniform(-10, 10, f.shape)
         return Workload("cfg1_256x256_rects_rho3_N5", _stack(f), _stack(theta), _stack(sigma), 3, 5)
     if cfg == 2:
         H, W = max(16, int(450 * scale)), max(16, int(600 * scale))
-        f = texture(H, W, 1000 * cfg)
+        f = texture(H, W, seed)
         rng11 = ndimage.maximum_filter(f, size=11, mode="reflect") - ndimage.minimum_filter(
             f, size=11, mode="reflect")
         sigma = 5.0 + 2.5 * rng11
@@ -137,7 +146,7 @@ def config(cfg: int, scale: float = 1.0) -> Workload:
         return Workload("cfg2_600x450_texture_rho5_N6", _stack(f), _stack(theta), _stack(sigma), 5, 6)
     if cfg == 3:
         H, W = max(32, int(1080 * scale)), max(32, int(1920 * scale))
-        f = voronoi(H, W, 1000 * cfg, n_seeds=64, noise_sd=15.0)
+        f = voronoi(H, W, seed, n_seeds=64, noise_sd=15.0)
         L = -ndimage.gaussian_laplace(f.astype(np.float64), 2.0, mode="reflect", truncate=4.0)
         tl = np.tanh(L / 10.0)
         theta = f + 20.0 * tl
@@ -145,8 +154,8 @@ def config(cfg: int, scale: float = 1.0) -> Workload:
         return Workload("cfg3_1920x1080_voronoi64_rho10_N8", _stack(f), _stack(theta), _stack(sigma), 10, 8)
     if cfg == 4:
         H, W = max(64, int(2160 * scale)), max(64, int(3840 * scale))
-        f = voronoi(H, W, 1000 * cfg, n_seeds=256, noise_sd=20.0)
-        rng = np.random.default_rng(1000 * cfg + 500)
+        f = voronoi(H, W, seed, n_seeds=256, noise_sd=20.0)
+        rng = np.random.default_rng(seed + 500)
         sigma = rng.uniform(5, 60, f.shape)
         theta = f + rng.uniform(-15, 15, f.shape)
         return Workload("cfg4_3840x2160_voronoi256_rho20_N8", _stack(f), _stack(theta), _stack(sigma), 20, 8)
