@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <new>
 #include <string>
 #include <vector>
@@ -1378,7 +1379,12 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               for (int e = 0; e < E; ++e) row0[e] = v0[e] + e0;
             }
           }
-        } else
+        } else {
+        // 1.0 where the shuffle has a source lane (sl >= off), else 0.0: one
+        // DFMA per round instead of a DADD under two selects
+        double fo[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fo[k] = (sl >= (1 << k)) ? 1.0 : 0.0;
         for (int b = 2 * warp; b < nr * N; b += 2 * G) {
           const int s0 = b + (sgrp & 1), s1r = s0 + G;
           const bool act0 = s0 < nr * N, act1 = s1r < nr * N;
@@ -1400,13 +1406,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           }
           double i0 = t0, i1 = t1;
 #pragma unroll
-          for (int off = 1; off < kSL; off <<= 1) {
-            const double u0 = __shfl_up_sync(0xffffffffu, i0, off, kSL);
-            const double u1v = __shfl_up_sync(0xffffffffu, i1, off, kSL);
-            if (sl >= off) {
-              i0 += u0;
-              i1 += u1v;
-            }
+          for (int k = 0; k < 4; ++k) {
+            const double u0 = __shfl_up_sync(0xffffffffu, i0, 1 << k, kSL);
+            const double u1v = __shfl_up_sync(0xffffffffu, i1, 1 << k, kSL);
+            i0 = fma(u0, fo[k], i0);
+            i1 = fma(u1v, fo[k], i1);
           }
           // the offset comes straight from the neighbour (never inc - tot: a
           // lane whose chunk runs into the padding carries garbage in tot)
@@ -1421,6 +1425,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
 #pragma unroll
             for (int e = 0; e < E; ++e) row1[e] = v1[e] + e1;
           }
+        }
         }
       }
       // horizontal bounds over VX, per (row r, block jb of w
@@ -1554,10 +1559,17 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // ---- phase C2: integrals, ratio, guard, store (one regime per warp).  No
       // ---- barrier after it (the counters are double buffered; the queue is
       // ---- read before the barrier that ends the next step's phase A).
-      {
+      // (the diagnostics' per-record work is compiled into a second copy of
+      // the loop: the product path tests no diagnostic pointer per record)
+      auto c2 = [&](auto diag_tag) {
+        constexpr bool D = decltype(diag_tag)::value;
         const int nA = cnt[qb] & 0xffff, nBC = cnt[qb] >> 16;
         const int rowbase = (int)plane + Yb * W + x0;
+#ifdef FABF_C2_UNROLL1
 #pragma unroll 1
+#else
+#pragma unroll
+#endif
         for (int i = 0; i < PPT; ++i) {
           const int j = tid + i * kThreads;
           if (j < nA || j >= QS - nBC) {
@@ -1579,17 +1591,21 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               float lam, t0;
               regime = range_params(al, be, th, sg, lam, t0);
             }
-            PixelResult res = ghat_from_record<N, true>(nu, QS, th, sg, al, be, regime, a.flags, want_t2n, n, s_etab,
-                                                                want_kappa);
+            PixelResult res = ghat_from_record<N, true>(nu, QS, th, sg, al, be, regime, a.flags, D && want_t2n, n,
+                                                        s_etab, D && want_kappa);
             a.out[o] = res.g;
-            if (want_diag) {
+            if constexpr (D) {
               if (a.d_kappa) a.d_kappa[o] = res.kappa;
               if (a.d_t2n) a.d_t2n[o] = res.t2n;
               if (a.d_code) a.d_code[o] = (unsigned char)res.code;
             }
           }
         }
-      }
+      };
+      if (want_diag)
+        c2(std::true_type{});
+      else
+        c2(std::false_type{});
       EXP_T(5);
     }
   }

@@ -50,6 +50,36 @@ __device__ __forceinline__ double poly_horner(const double* c, double x) {
   return p;
 }
 
+// The same polynomial as WAYS interleaved Horner chains in x^WAYS:
+// p(x) = sum_r x^r E_r(x^WAYS), r < WAYS.  Same operation count (+ the powers),
+// 1/WAYS of the dependent depth: C2 is bound by the fp64 pipe's latency at the
+// occupancy its registers allow, not by its throughput.
+#ifndef FABF_ERFCX_WAYS
+#define FABF_ERFCX_WAYS 1
+#endif
+template <int DEG, int WAYS>
+__device__ __forceinline__ double poly_split(const double* c, double x) {
+  if constexpr (WAYS == 1) {
+    return poly_horner<DEG>(c, x);
+  } else {
+    double xp[WAYS + 1];
+    xp[0] = 1.0;
+    xp[1] = x;
+#pragma unroll
+    for (int r = 2; r <= WAYS; ++r) xp[r] = xp[r / 2] * xp[r - r / 2];
+    double acc = 0.0;
+#pragma unroll
+    for (int r = WAYS - 1; r >= 0; --r) {
+      const int top = r + ((DEG - r) / WAYS) * WAYS;  // highest index = r mod WAYS
+      double e = c[top];
+#pragma unroll
+      for (int j = top - WAYS; j >= 0; j -= WAYS) e = fma(e, xp[WAYS], c[j]);
+      acc = (r == 0) ? acc + e : fma(e, xp[r], acc);
+    }
+    return acc;
+  }
+}
+
 // 1/d for normal positive d: MUFU.RCP64H seed + two Newton steps (relative
 // error ~1e-16, no special-case branches: d is in [1, 1e4] here).
 __device__ __forceinline__ double rcp64(double d) {
@@ -90,7 +120,7 @@ __device__ __forceinline__ double exp_nonpos(double z) {
 __constant__ double c_exp2_64[64];
 __device__ __forceinline__ double exp_nonpos_tab(double z, const double* __restrict__ tab) {
   const double kShift = 6755399441055744.0;  // 1.5 * 2^52
-  const double zc = fmax(z, -708.0);
+  const double zc = z < -708.0 ? -708.0 : z;  // (a select: fmax's NaN handling costs 4 more)
   const double ks = fma(zc, 92.33248261689366, kShift);
   const double kd = ks - kShift;
   double r = fma(kd, -0.01083042469326756, zc);  // ln2/64, 32 significant bits: kd * hi exact
