@@ -19,6 +19,9 @@ from .oracle import (  # noqa: F401
     mozerov,
     sharpen_maps,
     SHARPEN_DEFAULTS,
+    texture_maps,
+    texture_pipeline,
+    TEXTURE_DEFAULTS,
     stretch,
     CODE_IDENTITY,
     CODE_GUARD,

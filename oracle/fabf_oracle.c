@@ -794,3 +794,50 @@ int fabfo_sharpen_maps(const float* img, int B, int H, int W, int rho, double s,
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-2, second application: texture filtering.                   */
+/*   mRTV(i) = Delta(i) max_{j in W_i} |grad f(j)| / (sum_{j in W_i} |grad f(j)| + eps)   */
+/*   Delta(i) = max_{j in W_i} f(j) - min_{j in W_i} f(j) */
+/*   sigma(i) = an affine map of mRTV(i), high where mRTV is low    */
+/* The paper fixes neither W_i, the gradient stencil, eps nor the map; reading */
+/* R19: W_i = the box of half-width `patch` around i; grad f(j) =   */
+/* forward differences (f(y, x+1) - f(y, x), f(y+1, x) - f(y, x)) with the      */
+/* image reflected at its borders (reading R2: the difference across the last  */
+/* column / row is 0), |.| the Euclidean norm; a window position j outside the */
+/* image takes the value of the pixel it reflects to;                          */
+/*   sigma = s_hi - (s_hi - s_lo) min(mRTV / m_sat, 1).                        */
+/* Direct window scans per pixel, fp64 (the sum in __float128).               */
+static double grad_mag(const float* base, long H, long W, long y, long x) {
+  const double f = base[y * W + x];
+  const double gx = (double)base[y * W + reflect_index(x + 1, W)] - f;
+  const double gy = (double)base[reflect_index(y + 1, H) * W + x] - f;
+  return sqrt(gx * gx + gy * gy);
+}
+
+int fabfo_texture_maps(const float* img, int B, int H, int W, int patch, double s_lo, double s_hi, double m_sat,
+                       double eps, long p0, long p1, double* mrtv, double* sigma) {
+  if (!img || !mrtv || !sigma || B < 1 || H < 1 || W < 1 || patch < 0 || !(m_sat > 0) || !(eps > 0)) return 1;
+  if (2 * patch + 1 > H || 2 * patch + 1 > W) return 1;
+  const long HW = (long)H * W;
+  for (long p = p0; p < p1; ++p) {
+    const long b = p / HW, rr = p % HW, y = rr / W, x = rr % W;
+    const float* base = img + b * HW;
+    double fmin_ = INFINITY, fmax_ = -INFINITY, gmax = 0.0;
+    qd gsum = 0;
+    for (long dy = -patch; dy <= patch; ++dy)
+      for (long dx = -patch; dx <= patch; ++dx) {
+        const long yy = reflect_index(y + dy, H), xx = reflect_index(x + dx, W);
+        const double f = base[yy * W + xx], g = grad_mag(base, H, W, yy, xx);
+        if (f < fmin_) fmin_ = f;
+        if (f > fmax_) fmax_ = f;
+        if (g > gmax) gmax = g;
+        gsum += g;
+      }
+    const double m = (fmax_ - fmin_) * gmax / ((double)gsum + eps);
+    mrtv[p] = m;
+    const double u = m / m_sat;
+    sigma[p] = s_hi - (s_hi - s_lo) * (u < 1.0 ? u : 1.0);
+  }
+  return 0;
+}

@@ -60,8 +60,9 @@ def _load():
             lib.fabfo_brute_gauss.argtypes = [P, P, P, i, i, i, i, l, l, P]
             lib.fabfo_window_w.argtypes = [P, P, i, ctypes.c_float, ctypes.c_float, ctypes.c_float, i, i, P, P]
             lib.fabfo_sharpen_maps.argtypes = [P, i, i, i, i, d, d, d, d, l, l, P, P]
+            lib.fabfo_texture_maps.argtypes = [P, i, i, i, i, d, d, d, d, l, l, P, P]
             for fn in ("fabfo_bounds", "fabfo_brute", "fabfo_fast", "fabfo_window", "fabfo_literal", "fabfo_mozerov",
-                       "fabfo_sharpen_maps", "fabfo_fast_gauss", "fabfo_brute_gauss", "fabfo_window_w",
+                       "fabfo_sharpen_maps", "fabfo_texture_maps", "fabfo_fast_gauss", "fabfo_brute_gauss", "fabfo_window_w",
                        "fabfo_hilbert_inverse", "fabfo_fit", "fabfo_stretch", "fabfo_integrals"):
                 getattr(lib, fn).restype = ctypes.c_int
             _lib = lib
@@ -294,3 +295,59 @@ def sharpen_maps(img, rho: int, log_scale=1.0, sigma_lo=10.0, sigma_hi=40.0, log
 
     _parallel(f.size, run, threads, chunk=4096)
     return th.reshape(np.shape(img)), sg.reshape(np.shape(img))
+
+
+TEXTURE_DEFAULTS = dict(patch=3, sigma_lo=8.0, sigma_hi=50.0, mrtv_sat=12.0, eps=1e-3, second_scale=0.8)
+
+
+def texture_maps(img, patch=3, sigma_lo=8.0, sigma_hi=50.0, mrtv_sat=12.0, eps=1e-3, second_scale=0.8,
+                 threads: int | None = None):
+    """The texture-filtering application's maps (reading R19): mRTV over
+    the box of half-width ``patch`` and sigma = sigma_hi - (sigma_hi - sigma_lo)
+    min(mRTV / mrtv_sat, 1).  Returns (mrtv, sigma) as float64 (``second_scale``
+    belongs to the pipeline and is ignored here)."""
+    lib = _load()
+    f = _as3d(img)
+    B, H, W = f.shape
+    m = np.empty(f.shape, np.float64)
+    sg = np.empty(f.shape, np.float64)
+
+    def run(p0, p1):
+        if lib.fabfo_texture_maps(_ptr(f), B, H, W, int(patch), float(sigma_lo), float(sigma_hi), float(mrtv_sat),
+                                  float(eps), p0, p1, _ptr(m), _ptr(sg)):
+            raise ValueError("fabfo_texture_maps: invalid arguments")
+
+    _parallel(f.size, run, threads, chunk=4096)
+    return m.reshape(np.shape(img)), sg.reshape(np.shape(img))
+
+
+def texture_pipeline(img, rho: int, N: int, texture=None, sharpen=None, rho_sharpen: int | None = None,
+                     sigma=None, pass1=None, pass2=None, threads: int | None = None):
+    """The three applications of Algorithm 1 of P:849-852: smoothing with
+    theta = f and the mRTV sigma map, smoothing again with sigma scaled by
+    ``second_scale`` (0.8 in the paper; the map is still the input image's), then
+    the sharpening rule of P:620-630 on the result.  Each pass's output is the
+    guarded g-hat rounded to fp32 (it is the next pass's fp32 input image, as on
+    the device), the maps are rounded to fp32 likewise.  ``sigma`` / ``pass1`` /
+    ``pass2`` replace the corresponding intermediate when given (stage-by-stage
+    parity: the next stage is evaluated on the device's own intermediate).
+    Returns a dict: sigma, pass1, pass2, theta3, sigma3, out."""
+    tp = dict(TEXTURE_DEFAULTS)
+    tp.update(texture or {})
+    sp = dict(SHARPEN_DEFAULTS)
+    sp.update(sharpen or {})
+    rs = rho if rho_sharpen is None else int(rho_sharpen)
+    f = _f32(img)
+    if sigma is None:
+        sigma = texture_maps(f, threads=threads, **tp)[1]
+    sg = _f32(sigma)
+    if pass1 is None:
+        pass1 = fast(f, f, sg, rho, N, threads=threads)["g_guard"]
+    g1 = _f32(pass1)
+    sg2 = _f32(np.float32(tp["second_scale"]) * sg)
+    if pass2 is None:
+        pass2 = fast(g1, g1, sg2, rho, N, threads=threads)["g_guard"]
+    g2 = _f32(pass2)
+    th3, sg3 = sharpen_maps(g2, rs, threads=threads, **sp)
+    out = fast(g2, _f32(th3), _f32(sg3), rs, N, threads=threads)["g_guard"]
+    return dict(sigma=sg, pass1=g1, pass2=g2, theta3=th3, sigma3=sg3, out=out)

@@ -472,6 +472,89 @@ def test_sharpen_maps_against_scipy(orc, rho, s):
     assert sg.min() >= 8.0 and sg.max() <= 35.0
 
 
+# ---------------------------------------------------------------- NEXT-2: texture maps (mRTV)
+@pytest.mark.parametrize("patch", [1, 3, 5])
+def test_texture_maps_against_scipy(orc, patch):
+    """mRTV of P:835-842 (reading R19): the window max / min / sum come from
+    scipy's maximum_filter / minimum_filter / uniform_filter (reflect borders,
+    independent library routines) applied to f and to numpy's forward-difference
+    gradient magnitude; sigma is the stated affine map, clipped."""
+    w = workloads.random_case(2, 37, 45, seed=71, kind="texture", rho=2, N=0)
+    eps, m_sat = 1e-3, 9.0
+    m, sg = orc.texture_maps(w.img, patch=patch, sigma_lo=6.0, sigma_hi=44.0, mrtv_sat=m_sat, eps=eps)
+    for b in range(2):
+        f = w.img[b].astype(np.float64)
+        gx = np.diff(f, axis=1, append=f[:, -1:])
+        gy = np.diff(f, axis=0, append=f[-1:, :])
+        G = np.hypot(gx, gy)
+        k = 2 * patch + 1
+        delta = ndimage.maximum_filter(f, size=k, mode="reflect") - ndimage.minimum_filter(f, size=k, mode="reflect")
+        gmax = ndimage.maximum_filter(G, size=k, mode="reflect")
+        gsum = ndimage.uniform_filter(G, size=k, mode="reflect") * k * k
+        ref = delta * gmax / (gsum + eps)
+        assert np.max(np.abs(m[b] - ref)) < 1e-9 * max(1.0, ref.max())
+        rs = 44.0 - (44.0 - 6.0) * np.minimum(ref / m_sat, 1.0)
+        assert np.max(np.abs(sg[b] - rs)) < 1e-8
+    assert sg.min() >= 6.0 and sg.max() <= 44.0
+
+
+def test_texture_maps_closed_forms(orc):
+    """Closed forms that follow from the definition: a constant image
+    has mRTV = 0 (sigma = sigma_hi); a vertical step edge of height A has
+    mRTV = A * A / ((2p+1) A + eps) at every pixel whose window meets the edge
+    (Delta = A, one gradient sample of size A per window row); one-pixel vertical
+    stripes 0 / A have mRTV = A * A / (n A + eps) in the interior -- the texture
+    scores below the edge ("high near sharp edges and low in textured
+    regions"); mRTV is invariant to an intensity offset and, as eps -> 0,
+    proportional to an intensity scale."""
+    p, A, eps = 3, 60.0, 1e-6
+    n = (2 * p + 1) ** 2
+    c = np.full((1, 20, 24), 91.0, np.float32)
+    m, sg = orc.texture_maps(c, patch=p, sigma_lo=5.0, sigma_hi=33.0, mrtv_sat=4.0, eps=eps)
+    assert np.all(m == 0.0) and np.all(sg == 33.0)
+    e = np.zeros((1, 20, 24), np.float32)
+    e[:, :, 12:] = A
+    m, _ = orc.texture_maps(e, patch=p, eps=eps)
+    edge = A * A / ((2 * p + 1) * A + eps)
+    # forward difference: the gradient sample sits at column 11; windows of columns 8..14 contain it,
+    # of which columns 9..14 also see both levels (column 8's window is columns 5..11: flat, Delta = 0)
+    assert np.allclose(m[0, :, 9:15], edge, rtol=1e-12)
+    assert np.all(m[0, :, :9] == 0.0) and np.all(m[0, :, 15:] == 0.0)
+    s = np.zeros((1, 20, 24), np.float32)
+    s[:, :, 1::2] = A
+    m, _ = orc.texture_maps(s, patch=p, eps=eps)
+    tex = A * A / (n * A + eps)
+    assert np.allclose(m[0, 4:-4, 4:-5], tex, rtol=1e-12)
+    assert tex < edge
+    w = workloads.random_case(1, 25, 31, seed=72, kind="rect", rho=2, N=0)
+    m0, _ = orc.texture_maps(w.img, patch=2, eps=1e-12)
+    m1, _ = orc.texture_maps(w.img + 17.0, patch=2, eps=1e-12)
+    m2, _ = orc.texture_maps(w.img * 0.5, patch=2, eps=1e-12)
+    assert np.allclose(m1, m0, rtol=1e-9, atol=1e-9) and np.allclose(m2, 0.5 * m0, rtol=1e-9, atol=1e-9)
+
+
+def test_texture_pipeline_composition(orc):
+    """the pipeline is three applications of Algorithm 1 -- checked
+    here against the three oracle calls made one by one (theta = f, sigma; then
+    theta = g1, 0.8 sigma with the same map; then the sharpening maps of g2),
+    and on a constant image every pass is the identity."""
+    w = workloads.random_case(1, 30, 34, seed=73, kind="texture", rho=3, N=3)
+    tp = dict(patch=2, sigma_lo=7.0, sigma_hi=30.0, mrtv_sat=10.0, eps=1e-3, second_scale=0.8)
+    sp = dict(log_scale=1.0, sigma_lo=9.0, sigma_hi=25.0, log_sat=15.0)
+    r = orc.texture_pipeline(w.img, 3, 3, texture=tp, sharpen=sp, rho_sharpen=2)
+    sg = orc.texture_maps(w.img, **tp)[1].astype(np.float32)
+    g1 = orc.fast(w.img, w.img, sg, 3, 3)["g_guard"].astype(np.float32)
+    g2 = orc.fast(g1, g1, (np.float32(0.8) * sg).astype(np.float32), 3, 3)["g_guard"].astype(np.float32)
+    th3, sg3 = orc.sharpen_maps(g2, 2, **sp)
+    out = orc.fast(g2, th3.astype(np.float32), sg3.astype(np.float32), 2, 3)["g_guard"]
+    assert np.array_equal(r["pass1"], g1) and np.array_equal(r["pass2"], g2) and np.array_equal(r["out"], out)
+    # smoothing passes shrink the texture's variance, the structure survives (mean level kept)
+    assert r["pass2"].std() < w.img.std() and abs(float(r["pass2"].mean() - w.img.mean())) < 2.0
+    c = np.full((1, 16, 18), 40.0, np.float32)
+    rc = orc.texture_pipeline(c, 2, 2)
+    assert np.all(rc["out"] == 40.0)
+
+
 # ---------------------------------------------------------------- NEXT-1: Gaussian omega, eq.(4)
 def _gauss_w(rho):
     R = 3 * rho
