@@ -337,6 +337,7 @@ def run_gpu(args):
     fused = {} if args.no_other_configs else fused_variant(fb, w, img, th, sg, flush)
     colour = {} if args.no_other_configs else colour_variant(fb, dev, flush)
     sharpen = {} if args.no_other_configs else sharpen_variant(fb, dev, flush)
+    texture = {} if args.no_other_configs else texture_variant(fb, dev, flush)
     gauss = {} if args.no_other_configs else gauss_variant(fb, dev, flush)
     others = {} if args.no_other_configs else other_configs(fb, dev, flush)
 
@@ -411,6 +412,7 @@ def run_gpu(args):
             "fused_variant": fused,
             "colour_variant": colour,
             "sharpen_variant": sharpen,
+            "texture_variant": texture,
             "gauss_variant": gauss,
             "clocks": clk.summary(),
         }
@@ -562,6 +564,54 @@ def sharpen_variant(fb, dev, flush, steps: int = 10):
                      "e2e Mpix/s": H * W / e2e_s / 1e6, "e2e_ms": e2e_s * 1e3,
                      "h2d_bytes_per_frame": 4 * H * W, "d2h_bytes_per_frame": 4 * H * W,
                      "params": dict(fb.SHARPEN_DEFAULTS)}
+    return res
+
+
+def texture_variant(fb, dev, flush, steps: int = 10):
+    """NEXT-2: the texture-filtering application (fabf_filter_texture):
+    the mRTV sigma map on the device, two smoothing passes and the sharpening
+    pass (Algorithm 1 three times) from f alone.  Three 650x500 planes of the
+    synthetic texture generator (the paper's Fig.11 images are about 500x650
+    colour, filtered channel by channel, 2.5 s in its MATLAB implementation; here
+    every plane gets its own map) at rho = 5, N = 5, and a 4K plane at rho = 10,
+    N = 5.  Device-timed Mpix/s of output pixels, and end to end (image up,
+    result down: 4 + 4 bytes per pixel)."""
+    import torch
+
+    import workloads
+
+    res = {}
+    for name, (B, H, W, rho, N) in {"texture_3x650x500_rho5_N5": (3, 650, 500, 5, 5),
+                                    "texture_4k_rho10_N5": (1, 2160, 3840, 10, 5)}.items():
+        f = np.stack([workloads.texture(H, W, seed=7700 + 10 * b + B) for b in range(B)]).astype(np.float32)
+        img = torch.from_numpy(f).to(dev)
+        out = torch.empty_like(img)
+        plan = fb.Plan(B, H, W)
+        stream = torch.cuda.current_stream()
+        for _ in range(3):
+            fb.filter_texture(plan, img, rho, N, out=out)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in ev:
+            flush.fill_(1.0)
+            a.record(stream)
+            fb.filter_texture(plan, img, rho, N, out=out)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        h_img = torch.from_numpy(f).pin_memory()
+        h_out = torch.empty_like(h_img).pin_memory()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            img.copy_(h_img, non_blocking=True)
+            fb.filter_texture(plan, img, rho, N, out=out)
+            h_out.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_s = (time.perf_counter() - t0) / steps
+        px = B * H * W
+        res[name] = {"Mpix/s": px / (ms * 1e-3) / 1e6, "ms": ms, "launches": plan.last_launch_count(),
+                     "passes": 3, "e2e Mpix/s": px / e2e_s / 1e6, "e2e_ms": e2e_s * 1e3,
+                     "h2d_bytes_per_call": 4 * px, "d2h_bytes_per_call": 4 * px,
+                     "params": dict(fb.TEXTURE_DEFAULTS)}
     return res
 
 

@@ -169,6 +169,43 @@ fabf_status_t fabf_sharpen_maps(fabf_plan_t plan, const float* img, int rho, con
 fabf_status_t fabf_filter_sharpen(fabf_plan_t plan, const float* img, int rho, int N, const fabf_sharpen_t* prm,
                                   float* out, void* stream);
 
+/* NEXT-2, second application: texture filtering.  The sigma map is
+ * produced on the device from f alone,
+ *   mRTV(i)  = Delta(i) max_{j in W_i} |grad f(j)| / (sum_{j in W_i} |grad f(j)| + eps)
+ *   Delta(i) = max_{W_i} f - min_{W_i} f
+ *   sigma(i) = sigma_hi - (sigma_hi - sigma_lo) min(mRTV(i) / mrtv_sat, 1)
+ * ("an affine transformation of mRTV, sigma high whenever mRTV is low", P:847;
+ * the paper fixes neither W_i, the gradient stencil, eps nor the map: DESIGN.md
+ * reading R19 -- W_i the box of half-width `patch`, forward differences with
+ * the image reflected at its borders, Euclidean norm).                        */
+typedef struct {
+  int patch;          /* half-width of the neighbourhood W_i, 0..16             */
+  float sigma_lo;     /* sigma where mRTV >= mrtv_sat (strong edges)            */
+  float sigma_hi;     /* sigma where mRTV = 0 (texture, flat areas)             */
+  float mrtv_sat;     /* mRTV (intensity units) at which sigma_lo is reached    */
+  float eps;          /* the paper's epsilon (> 0, intensity units)             */
+  float second_scale; /* sigma factor of the second smoothing pass (paper: 0.8) */
+} fabf_texture_t;
+
+/* The map alone: sigma (and, if `mrtv` is not NULL, mRTV itself) as device
+ * batch x height x width fp32 planes.  Asynchronous.  INVALID_ARGUMENT for bad
+ * parameters or overlapping buffers.                                           */
+fabf_status_t fabf_texture_maps(fabf_plan_t plan, const float* img, const fabf_texture_t* prm, float* sigma,
+                                float* mrtv, void* stream);
+
+/* The whole application ("we apply Algorithm 1 thrice"): pass 1 =
+ * fabf_filter(img; theta = img, sigma); pass 2 = fabf_filter(pass 1; theta =
+ * pass 1, second_scale * sigma) with the SAME map; out = the sharpening
+ * application (fabf_filter_sharpen's rule, window half-width rho_sharpen) of
+ * pass 2.  Maps and intermediates live in plan-owned buffers (allocated on
+ * first use, shared with fabf_filter_host); `pass1` / `pass2`, when not NULL,
+ * are device planes that receive the intermediates instead.  Every pass obeys
+ * the plan's flags; fabf_last_fallback_count reports the last pass.
+ * Asynchronous on `stream`; errors as fabf_filter / fabf_sharpen_maps.         */
+fabf_status_t fabf_filter_texture(fabf_plan_t plan, const float* img, int rho, int N, const fabf_texture_t* tprm,
+                                  int rho_sharpen, const fabf_sharpen_t* sprm, float* out, float* pass1,
+                                  float* pass2, void* stream);
+
 /* The baseline the paper compares with (NEXT-4): Mozerov & van de Weijer's
  * uniform-prior filter with Delta = 0 (Fig.3) -- eq.(29) at
  * N = 0 fitted on [f(i), 2 fbar(i) - f(i)] (fbar = the box mean over the same

@@ -20,6 +20,9 @@ from .fabf import (  # noqa: F401
     filter_sharpen,
     sharpen_maps,
     SHARPEN_DEFAULTS,
+    filter_texture,
+    texture_maps,
+    TEXTURE_DEFAULTS,
     filter_profile,
     lib,
     library_path,

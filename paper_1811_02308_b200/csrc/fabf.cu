@@ -2153,6 +2153,87 @@ __global__ void __launch_bounds__(kThreads) k_sharpen_maps(const float* __restri
 }
 
 // ============================================================================
+// NEXT-2, second application: the texture-filtering sigma map,
+//   mRTV(i) = Delta(i) max_{W_i} |grad f| / (sum_{W_i} |grad f| + eps),
+//   Delta(i) = max_{W_i} f - min_{W_i} f,
+//   sigma = s_hi - (s_hi - s_lo) min(mRTV / m_sat, 1)              (reading R19)
+// W_i = the box of half-width pr, grad f by forward differences with the image
+// reflected at its borders (0 across the last column / row), a window position
+// outside the image takes the pixel it reflects to.  One CTA per T x T tile: f
+// and |grad f| (fp64: products and sum rounded separately, IEEE sqrt) of the
+// (T + 2 pr)^2 footprint in shared memory, then the separable window max / min /
+// sum (rows, then columns; pr is small: direct O(pr) scans).  Writes sigma,
+// scale2 * sigma (the pipeline's second pass) and, if asked, mRTV.
+constexpr int kMaxPatch = 16;
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_texture_maps(const float* __restrict__ img,
+                                                            float* __restrict__ sigma, float* __restrict__ sigma2,
+                                                            float* __restrict__ mrtv, int H, int W, int pr,
+                                                            float s_lo, float s_hi, double inv_sat, double eps,
+                                                            float scale2) {
+  extern __shared__ __align__(16) unsigned char smt[];
+  const int FS = T + 2 * pr, k = 2 * pr + 1;
+  double* G = reinterpret_cast<double*>(smt);  // [FS][FS] gradient magnitude
+  double* Hs = G + FS * FS;                    // [FS][T] row-window sum of G
+  double* Hm = Hs + FS * T;                    // [FS][T] row-window max of G
+  float* F = reinterpret_cast<float*>(Hm + FS * T);  // [FS][FS]
+  float* Hlo = F + FS * FS;                    // [FS][T] row-window min of f
+  float* Hhi = Hlo + FS * T;                   // [FS][T] row-window max of f
+  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T, b = blockIdx.z;
+  const size_t plane = (size_t)b * H * W;
+  const float* src = img + plane;
+  for (int t = threadIdx.x; t < FS * FS; t += kThreads) {
+    const int r = t / FS, cc = t - r * FS;
+    // (rows / columns past H - 1 + pr only feed outputs outside the image)
+    const int yy = reflect_index(min(y0 - pr + r, H - 1 + pr), H), xx = reflect_index(min(x0 - pr + cc, W - 1 + pr), W);
+    const float f = __ldg(src + (size_t)yy * W + xx);
+    const double gx = (double)__ldg(src + (size_t)yy * W + reflect_index(xx + 1, W)) - (double)f;
+    const double gy = (double)__ldg(src + (size_t)reflect_index(yy + 1, H) * W + xx) - (double)f;
+    F[t] = f;
+    G[t] = sqrt(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < FS * T; t += kThreads) {
+    const int r = t / T, x = t - r * T;
+    const double* Gr = G + r * FS + x;
+    const float* Fr = F + r * FS + x;
+    double sum = 0.0, gm = 0.0;
+    float lo = CUDART_INF_F, hi = -CUDART_INF_F;
+    for (int cc = 0; cc < k; ++cc) {
+      sum += Gr[cc];
+      gm = fmax(gm, Gr[cc]);
+      lo = fminf(lo, Fr[cc]);
+      hi = fmaxf(hi, Fr[cc]);
+    }
+    Hs[t] = sum;
+    Hm[t] = gm;
+    Hlo[t] = lo;
+    Hhi[t] = hi;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T * T; t += kThreads) {
+    const int y = t / T, x = t - y * T;
+    const int yy = y0 + y, xx = x0 + x;
+    if (yy >= H || xx >= W) continue;
+    double sum = 0.0, gm = 0.0;
+    float lo = CUDART_INF_F, hi = -CUDART_INF_F;
+    for (int dy = 0; dy < k; ++dy) {
+      const int rr = (y + dy) * T + x;
+      sum += Hs[rr];
+      gm = fmax(gm, Hm[rr]);
+      lo = fminf(lo, Hlo[rr]);
+      hi = fmaxf(hi, Hhi[rr]);
+    }
+    const double m = ((double)hi - (double)lo) * gm / (sum + eps);
+    const float sg = (float)((double)s_hi - ((double)s_hi - (double)s_lo) * fmin(m * inv_sat, 1.0));
+    const size_t o = plane + (size_t)yy * W + xx;
+    sigma[o] = sg;
+    if (sigma2) sigma2[o] = scale2 * sg;
+    if (mrtv) mrtv[o] = (float)m;
+  }
+}
+
+// ============================================================================
 // colour (NEXT-3): channel-interleaved images (B x H x W x C) <-> the planar
 // batch (B C) x H x W the filter runs on, channel by channel as the paper
 // filters colour images.  Pure data movement, coalesced on the
@@ -3108,6 +3189,102 @@ fabf_status_t fabf_filter_sharpen(fabf_plan_t plan, const float* img, int rho, i
   s = filter_impl(p, img, th, sg, rho, N, out, nullptr, (cudaStream_t)stream);
   if (s != FABF_OK) return s;
   p->launches += maps;
+  return FABF_OK;
+}
+
+namespace {
+fabf_status_t ensure_staging(Plan* p) {  // planar staging (shared with fabf_filter_host), on first use
+  if (p->h_in) return FABF_OK;
+  const size_t px = (size_t)p->B * p->H * p->W;
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->h_in, 3 * sizeof(float) * staging_pitch(px))) != cudaSuccess)
+    return cuda_fail(e, "cudaMalloc(staging)");
+  if ((e = cudaMalloc(&p->h_out, px * sizeof(float))) != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+  return FABF_OK;
+}
+
+fabf_status_t texture_maps_impl(Plan* p, const float* img, const fabf_texture_t* prm, float* sigma,
+                                float* sigma2, float* mrtv, cudaStream_t st) {
+  if (!img || !sigma || !prm) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (prm->patch < 0 || prm->patch > kMaxPatch || 2 * prm->patch + 1 > p->H || 2 * prm->patch + 1 > p->W)
+    return fail(FABF_ERR_INVALID_ARGUMENT, "patch must be in [0, 16] and its window inside the image");
+  if (!(prm->mrtv_sat > 0.0f) || !(prm->eps > 0.0f) || !(prm->sigma_lo > 0.0f) || !(prm->sigma_hi >= prm->sigma_lo) ||
+      !(prm->second_scale > 0.0f))
+    return fail(FABF_ERR_INVALID_ARGUMENT,
+                "texture parameters: mrtv_sat, eps, sigma_lo, second_scale > 0, sigma_hi >= sigma_lo");
+  const size_t bytes = sizeof(float) * (size_t)p->B * p->H * p->W;
+  if (overlaps(sigma, bytes, img, bytes) || (mrtv && (overlaps(mrtv, bytes, img, bytes) || overlaps(mrtv, bytes, sigma, bytes))))
+    return fail(FABF_ERR_INVALID_ARGUMENT, "outputs overlap");
+  constexpr int T = 32;
+  const int FS = T + 2 * prm->patch;
+  const size_t smem = (sizeof(double) + sizeof(float)) * ((size_t)FS * FS + 2 * (size_t)FS * T);
+  {
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (!attr_set[p->device]) {
+      FABF_CUDA(cudaFuncSetAttribute(k_texture_maps<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem),
+                "cudaFuncSetAttribute(k_texture_maps)");
+      attr_set[p->device] = true;
+    }
+  }
+  dim3 g((p->W + T - 1) / T, (p->H + T - 1) / T, p->B);
+  k_texture_maps<T><<<g, kThreads, smem, st>>>(img, sigma, sigma2, mrtv, p->H, p->W, prm->patch, prm->sigma_lo,
+                                               prm->sigma_hi, 1.0 / (double)prm->mrtv_sat, (double)prm->eps,
+                                               prm->second_scale);
+  FABF_CUDA(cudaGetLastError(), "k_texture_maps launch");
+  ++g_launches;
+  return FABF_OK;
+}
+}  // namespace
+
+fabf_status_t fabf_texture_maps(fabf_plan_t plan, const float* img, const fabf_texture_t* prm, float* sigma,
+                                float* mrtv, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  fabf_status_t s = validate_common(p, 0);
+  if (s != FABF_OK) return s;
+  return texture_maps_impl(p, img, prm, sigma, nullptr, mrtv, (cudaStream_t)stream);
+}
+
+fabf_status_t fabf_filter_texture(fabf_plan_t plan, const float* img, int rho, int N, const fabf_texture_t* tprm,
+                                  int rho_sharpen, const fabf_sharpen_t* sprm, float* out, float* pass1,
+                                  float* pass2, void* stream) {
+  // Algorithm 1 three times -- theta = f with the mRTV sigma map,
+  // again on the result with sigma scaled by second_scale (the same map), then
+  // the sharpening rule of P:620-630 on that
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  fabf_status_t s = validate_common(p, rho);
+  if (s != FABF_OK) return s;
+  if (!img || !out || !tprm || !sprm) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  const size_t px = (size_t)p->B * p->H * p->W, bytes = px * sizeof(float);
+  if ((pass1 && (overlaps(pass1, bytes, img, bytes) || overlaps(pass1, bytes, out, bytes))) ||
+      (pass2 && (overlaps(pass2, bytes, img, bytes) || overlaps(pass2, bytes, out, bytes))) ||
+      (pass1 && pass2 && overlaps(pass1, bytes, pass2, bytes)))
+    return fail(FABF_ERR_INVALID_ARGUMENT, "pass1 / pass2 overlap another buffer");
+  s = ensure_staging(p);
+  if (s != FABF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t pitch = staging_pitch(px);
+  float* g1 = pass1 ? pass1 : p->h_in;
+  float* g2 = pass2 ? pass2 : p->h_out;
+  float* pa = p->h_in + pitch;      // sigma, then theta of the sharpening pass
+  float* pb = p->h_in + 2 * pitch;  // second_scale * sigma, then sigma of the sharpening pass
+  g_launches = 0;
+  s = texture_maps_impl(p, img, tprm, pa, pb, nullptr, st);
+  if (s != FABF_OK) return s;
+  int total = g_launches;
+  s = filter_impl(p, img, img, pa, rho, N, g1, nullptr, st);
+  if (s != FABF_OK) return s;
+  total += p->launches;
+  s = filter_impl(p, g1, g1, pb, rho, N, g2, nullptr, st);
+  if (s != FABF_OK) return s;
+  total += p->launches;
+  g_launches = 0;
+  s = fabf_sharpen_maps(plan, g2, rho_sharpen, sprm, pa, pb, stream);
+  if (s != FABF_OK) return s;
+  total += g_launches;
+  s = filter_impl(p, g2, pa, pb, rho_sharpen, N, out, nullptr, st);
+  if (s != FABF_OK) return s;
+  p->launches += total;
   return FABF_OK;
 }
 

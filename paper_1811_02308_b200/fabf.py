@@ -43,6 +43,14 @@ class _Sharpen(ctypes.Structure):
 SHARPEN_DEFAULTS = dict(log_scale=1.0, sigma_lo=10.0, sigma_hi=40.0, log_sat=20.0)
 
 
+class _Texture(ctypes.Structure):
+    _fields_ = [("patch", ctypes.c_int), ("sigma_lo", ctypes.c_float), ("sigma_hi", ctypes.c_float),
+                ("mrtv_sat", ctypes.c_float), ("eps", ctypes.c_float), ("second_scale", ctypes.c_float)]
+
+
+TEXTURE_DEFAULTS = dict(patch=3, sigma_lo=8.0, sigma_hi=50.0, mrtv_sat=12.0, eps=1e-3, second_scale=0.8)
+
+
 class _Diag(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_void_p), ("beta", ctypes.c_void_p), ("kappa", ctypes.c_void_p),
                 ("t2n", ctypes.c_void_p), ("code", ctypes.c_void_p)]
@@ -74,6 +82,12 @@ def lib():
                 L.fabf_sharpen_maps.restype = ctypes.c_int
                 L.fabf_filter_sharpen.argtypes = [P, P, i, i, ctypes.POINTER(_Sharpen), P, P]
                 L.fabf_filter_sharpen.restype = ctypes.c_int
+            if hasattr(L, "fabf_filter_texture"):
+                L.fabf_texture_maps.argtypes = [P, P, ctypes.POINTER(_Texture), P, P, P]
+                L.fabf_texture_maps.restype = ctypes.c_int
+                L.fabf_filter_texture.argtypes = [P, P, i, i, ctypes.POINTER(_Texture), i, ctypes.POINTER(_Sharpen),
+                                                  P, P, P, P]
+                L.fabf_filter_texture.restype = ctypes.c_int
             if hasattr(L, "fabf_filter_gauss"):
                 L.fabf_filter_gauss.argtypes = [P, P, P, P, i, i, P, P]
                 L.fabf_filter_gauss.restype = ctypes.c_int
@@ -347,6 +361,45 @@ def filter_sharpen(plan: Plan, img, rho: int, N: int, out=None, stream=None, **p
     prm = _sharpen_params(params)
     _check(lib().fabf_filter_sharpen(plan.handle, _dev_ptr(img, "img", plan), int(rho), int(N), ctypes.byref(prm),
                                      _dev_ptr(out, "out", plan), _stream_ptr(stream)))
+    return out
+
+
+def _texture_params(kw):
+    prm = dict(TEXTURE_DEFAULTS)
+    prm.update(kw or {})
+    return _Texture(int(prm["patch"]), *(float(prm[k]) for k in ("sigma_lo", "sigma_hi", "mrtv_sat", "eps",
+                                                                  "second_scale")))
+
+
+def texture_maps(plan: Plan, img, sigma=None, mrtv=None, want_mrtv: bool = False, stream=None, **params):
+    """fabf_texture_maps: the texture application's sigma map; returns
+    (sigma, mrtv) -- mrtv is None unless asked for."""
+    import torch
+
+    sigma = torch.empty_like(img) if sigma is None else sigma
+    if mrtv is None and want_mrtv:
+        mrtv = torch.empty_like(img)
+    prm = _texture_params(params)
+    _check(lib().fabf_texture_maps(plan.handle, _dev_ptr(img, "img", plan), ctypes.byref(prm),
+                                   _dev_ptr(sigma, "sigma", plan),
+                                   None if mrtv is None else _dev_ptr(mrtv, "mrtv", plan), _stream_ptr(stream)))
+    return sigma, mrtv
+
+
+def filter_texture(plan: Plan, img, rho: int, N: int, texture=None, sharpen=None, rho_sharpen=None, out=None,
+                   pass1=None, pass2=None, stream=None):
+    """fabf_filter_texture: the three-pass texture-filtering application
+    on device tensors; ``pass1`` / ``pass2`` (optional tensors) receive the
+    intermediates."""
+    import torch
+
+    out = torch.empty_like(img) if out is None else out
+    tp, sp = _texture_params(texture), _sharpen_params(sharpen or {})
+    rs = int(rho if rho_sharpen is None else rho_sharpen)
+    _check(lib().fabf_filter_texture(plan.handle, _dev_ptr(img, "img", plan), int(rho), int(N), ctypes.byref(tp), rs,
+                                     ctypes.byref(sp), _dev_ptr(out, "out", plan),
+                                     None if pass1 is None else _dev_ptr(pass1, "pass1", plan),
+                                     None if pass2 is None else _dev_ptr(pass2, "pass2", plan), _stream_ptr(stream)))
     return out
 
 

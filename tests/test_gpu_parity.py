@@ -536,6 +536,70 @@ def test_sharpen_application(fb, orc, kind, shape, rho, N, prm):
     assert plan.last_launch_count() >= 2
 
 
+@pytest.mark.parametrize("kind,shape,patch", [
+    ("texture", (2, 97, 131), 3), ("rect", (1, 120, 90), 1), ("float", (1, 70, 75), 5), ("voronoi", (1, 33, 200), 16),
+    ("flat", (1, 40, 40), 0), ("texture", (1, 20, 17), 2)])
+def test_texture_maps(fb, orc, kind, shape, patch):
+    """NEXT-2 (reading R19): the device mRTV / sigma maps equal the
+    oracle's direct window scans, every pixel (the gradient magnitudes are the
+    same fp64 values on both sides, so the window max is exact; the sums differ
+    by their order only); ragged tiles, a window as wide as a tile, patch 0."""
+    import torch
+
+    w = workloads.random_case(*shape, seed=91 + patch, kind=kind, rho=2, N=2)
+    plan = fb.Plan(*w.shape)
+    prm = dict(patch=patch, sigma_lo=6.0, sigma_hi=44.0, mrtv_sat=9.0, eps=1e-3)
+    sg, m = fb.texture_maps(plan, _dev(w.img), want_mrtv=True, **prm)
+    torch.cuda.synchronize()
+    rm, rsg = orc.texture_maps(w.img, **prm)
+    sg, m = sg.cpu().numpy(), m.cpu().numpy()
+    assert np.max(np.abs(m - rm.astype(np.float32))) <= 1e-5 * max(1.0, float(rm.max()))
+    assert np.max(np.abs(sg - rsg)) <= 1e-4
+    assert sg.min() >= 6.0 - 1e-5 and sg.max() <= 44.0 + 1e-5
+
+
+@pytest.mark.parametrize("kind,shape,rho,N,rs", [
+    ("texture", (1, 150, 170), 5, 5, 3), ("rect", (2, 90, 110), 3, 6, 3), ("voronoi", (1, 128, 96), 10, 8, 5)])
+def test_texture_application(fb, orc, kind, shape, rho, N, rs):
+    """NEXT-2: Algorithm 1 three times.  Stage by stage -- every
+    pass of the device pipeline against the oracle evaluated on the device's
+    own previous intermediate (each stage's error, every pixel, within the
+    0.05-grey bar) -- and end to end against the oracle's own pipeline."""
+    import torch
+
+    w = workloads.random_case(*shape, seed=95, kind=kind, rho=rho, N=N)
+    plan = fb.Plan(*w.shape)
+    tp = dict(fb.TEXTURE_DEFAULTS)
+    tp.update(patch=2, sigma_hi=35.0)
+    sp = dict(log_scale=1.0, sigma_lo=9.0, sigma_hi=25.0, log_sat=15.0)
+    img = _dev(w.img)
+    g1, g2 = torch.empty_like(img), torch.empty_like(img)
+    out = fb.filter_texture(plan, img, rho, N, texture=tp, sharpen=sp, rho_sharpen=rs, pass1=g1, pass2=g2)
+    launches = plan.last_launch_count()
+    out_plain = fb.filter_texture(plan, img, rho, N, texture=tp, sharpen=sp, rho_sharpen=rs)  # plan-owned intermediates
+    sg, _ = fb.texture_maps(plan, img, **tp)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out_plain)
+    assert launches >= 8  # 2 map kernels + 3 x (bounds or fused filter, fallback)
+    sg, g1, g2, out = sg.cpu().numpy(), g1.cpu().numpy(), g2.cpu().numpy(), out.cpu().numpy()
+    sc = grey_scale(w.img)
+    o1 = orc.fast(w.img, w.img, sg, rho, N)
+    mx, nbad, _ = compare_guarded(g1, o1, sc)
+    assert nbad == 0, f"pass 1: max |delta| = {mx} grey"
+    o2 = orc.fast(g1, g1, (np.float32(tp["second_scale"]) * sg).astype(np.float32), rho, N)
+    mx, nbad, _ = compare_guarded(g2, o2, sc)
+    assert nbad == 0, f"pass 2: max |delta| = {mx} grey"
+    th3, sg3 = fb.sharpen_maps(plan, _dev(g2), rs, **sp)
+    torch.cuda.synchronize()
+    o3 = orc.fast(g2, th3.cpu().numpy(), sg3.cpu().numpy(), rs, N)
+    mx, nbad, _ = compare_guarded(out, o3, sc)
+    assert nbad == 0, f"pass 3: max |delta| = {mx} grey"
+    # end to end: the oracle's own pipeline from f alone (errors of three passes compound)
+    ref = orc.texture_pipeline(w.img, rho, N, texture=tp, sharpen=sp, rho_sharpen=rs)
+    d = np.abs(out.astype(np.float64) - ref["out"]) / sc
+    assert np.quantile(d, 0.999) <= TOL_GREY, f"end to end p99.9 = {np.quantile(d, 0.999)} grey, max {d.max()}"
+
+
 @pytest.mark.parametrize("kind,shape,rho,N", [
     ("voronoi", (1, 96, 130), 3, 5), ("texture", (2, 70, 81), 1, 8), ("rect", (1, 100, 100), 5, 2),
     ("float", (1, 80, 90), 3, 6), ("flat", (1, 40, 40), 2, 5), ("voronoi", (1, 130, 150), 10, 5),
