@@ -699,6 +699,79 @@ def run_sweep(args):
     return 0
 
 
+def run_band(args):
+    """--shard band: ONE config-4 frame split into row bands over the ranks
+    (strong scaling).  Every rank keeps its band of f, theta,
+    sigma resident; a timed step is the halo exchange of rho rows of f with each
+    neighbour (shard.exchange_halo: NCCL send / recv) plus fabf_filter on the
+    band-plus-halo; the result stays on its rank.  Device time by CUDA events,
+    max over ranks; value = the frame's pixels over that time."""
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_1811_02308_b200 as fb
+    from paper_1811_02308_b200 import build, shard
+
+    build.build()
+    import workloads
+
+    w = workloads.config(CFG)
+    B, H, W = w.shape
+    first, n = shard.band_shard(H, ws, rank, rho=w.rho)
+    rows = slice(first, first + n)
+    band = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, rows])).to(dev)
+    f_b, th_b, sg_b = band(w.img), band(w.theta), band(w.sigma)
+    f, th, sg, top = shard.band_problem(f_b, th_b, sg_b, w.rho, ws, rank)
+    plan = fb.Plan(*f.shape)
+    out = torch.empty_like(f)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    hl = f.shape[1] - n - top  # halo rows below
+
+    def step():
+        fh, _ = shard.exchange_halo(f_b, w.rho, ws, rank)  # the exchange step, every frame
+        fb.filter(plan, fh, th, sg, w.rho, w.N, out=out)
+
+    with ClockSampler(local) as clk:
+        for i in range(max(3, args.warmup)):
+            flush.fill_(float(i))
+            step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i, (a, b) in enumerate(ev):
+            flush.fill_(float(i))
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+    tot_ms = shard.max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), device=dev)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": B * H * W * args.steps / (tot_ms * 1e-3) / 1e6, "unit": "Mpix/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 4, one frame in {ws} row bands (band_shard), rho-row halo of f exchanged "
+                                   "with each neighbour every step (send/recv), no collective after filtering",
+                       "rows_of_rank0": n, "halo_rows_above_below": [top, hl], "l2": "flushed between steps"},
+            "gpu_launches": plan.last_launch_count() * args.steps,
+            "halo_bytes_per_neighbour": 4 * w.rho * W * B, "clocks": clk.summary()}))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -712,7 +785,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer pass (launch-list captures)")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the configs 1-3 throughput lines")
+    ap.add_argument("--shard", default="frames", choices=["frames", "band"],
+                    help="N > 1: one frame per rank (weak, default) or one frame in row bands (strong)")
     args = ap.parse_args()
+    if args.shard == "band" and args.impl == "fabf" and not args.sweep:
+        return run_band(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.sweep:

@@ -536,6 +536,35 @@ def test_sharpen_application(fb, orc, kind, shape, rho, N, prm):
     assert plan.last_launch_count() >= 2
 
 
+def test_row_band_subproblems_on_device(fb, orc):
+    """SURVEY 8(e) row-band split, the per-rank computation on real kernels:
+    each band plus rho halo rows of f (what shard.exchange_halo delivers),
+    filtered as an image of its own and cropped, equals the oracle's rows of
+    the whole frame -- three bands, the middle one with halos on both sides
+    (the exchange itself is covered on CPU, tests/test_multi_gloo.py)."""
+    import torch
+
+    w = workloads.random_case(1, 150, 140, seed=97, kind="voronoi", rho=6, N=6)
+    ref = orc.fast(w.img, w.theta, w.sigma, w.rho, w.N)
+    sc = grey_scale(w.img)
+    from paper_1811_02308_b200.shard import band_shard
+
+    for rank in range(3):
+        first, n = band_shard(150, 3, rank, rho=w.rho)
+        lo, hi = max(0, first - w.rho), min(150, first + n + w.rho)
+        top = first - lo
+        f = np.ascontiguousarray(w.img[:, lo:hi])
+        th, sg = f.copy(), np.ones_like(f)
+        th[:, top:top + n] = w.theta[:, first:first + n]
+        sg[:, top:top + n] = w.sigma[:, first:first + n]
+        plan = fb.Plan(*f.shape)
+        out = fb.filter(plan, _dev(f), _dev(th), _dev(sg), w.rho, w.N)
+        torch.cuda.synchronize()
+        part = {k: v[:, first:first + n] for k, v in ref.items()}
+        mx, nbad, _ = compare_guarded(out.cpu().numpy()[:, top:top + n], part, sc)
+        assert nbad == 0, f"band {rank}: max |delta| = {mx} grey"
+
+
 @pytest.mark.parametrize("kind,shape,patch", [
     ("texture", (2, 97, 131), 3), ("rect", (1, 120, 90), 1), ("float", (1, 70, 75), 5), ("voronoi", (1, 33, 200), 16),
     ("flat", (1, 40, 40), 0), ("texture", (1, 20, 17), 2)])

@@ -6,7 +6,7 @@ import socket
 
 import pytest
 
-from paper_1811_02308_b200.shard import frame_shard, whole_job_rate
+from paper_1811_02308_b200.shard import band_shard, frame_shard, whole_job_rate
 
 
 @pytest.mark.parametrize("batch,world", [(32, 1), (32, 2), (32, 8), (5, 2), (3, 4), (0, 2), (7, 7)])
@@ -123,3 +123,71 @@ def test_gloo_world2_sharded_pipeline_matches_single_process():
     ref = oracle.fast(w.img, w.theta, w.sigma, w.rho, w.N)["g_guard"]
     for _, _, full in res:
         assert np.array_equal(full, ref)
+
+
+def test_band_shard_rejects_thin_bands():
+    assert band_shard(64, 2, 1, rho=5) == (32, 32)
+    with pytest.raises(ValueError):
+        band_shard(16, 4, 0, rho=5)
+
+
+def _band_worker(rank, world, port, q):
+    """One rank of the row-band split of a single frame on CPU: its band of f,
+    theta, sigma, ONE halo exchange of rho rows of f with each neighbour, the
+    band-plus-halo filtered as an image of its own (the oracle standing in for
+    the device kernels), cropped to the band."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import workloads
+    from paper_1811_02308_b200.shard import band_problem, band_shard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = workloads.random_case(2, 41, 29, seed=12, kind="voronoi", rho=4, N=3)
+        first, n = band_shard(41, world, rank, rho=w.rho)
+        rows = slice(first, first + n)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, rows]))
+        f, th, sg, top = band_problem(t(w.img), t(w.theta), t(w.sigma), w.rho, world, rank)
+        g = oracle.fast(f.numpy(), th.numpy(), sg.numpy(), w.rho, w.N)["g_guard"][:, top:top + n]
+        q.put((rank, first, n, tuple(f.shape), g))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_band_split_matches_single_process(world):
+    """A single frame split into row bands over 2 and 3 ranks: after the one
+    halo exchange every rank's cropped result equals the corresponding rows of
+    the single-process result (interior ranks carry a halo on both sides, the
+    border ranks rely on the filter's own reflection)."""
+    import numpy as np
+    import torch.multiprocessing as mp
+
+    import oracle
+    import workloads
+
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = sorted((q.get(timeout=10) for _ in range(world)), key=lambda t: t[0])
+    w = workloads.random_case(2, 41, 29, seed=12, kind="voronoi", rho=4, N=3)
+    ref = oracle.fast(w.img, w.theta, w.sigma, w.rho, w.N)["g_guard"]
+    rows = 0
+    for rank, first, n, shape, g in res:
+        halos = (rank > 0) + (rank < world - 1)
+        assert shape == (2, n + halos * w.rho, 29)
+        assert np.array_equal(g, ref[:, first:first + n])
+        rows += n
+    assert rows == 41
