@@ -945,10 +945,11 @@ struct FilterSmem {
     const int w = L - TW + 1, XP = FB ? xpitch(L, TW, w) : 0, YP = FB ? ypitch(TW, w) : 0;
     using G = FilterGeom<N, E>;
     size_t off = 0;
+    // the arrays whose size is a compile-time constant come first: their
+    // addresses are immediates in the kernel (no per-use pointer arithmetic
+    // from the run-time strip width L)
     ps = off;
     off += sizeof(double) * (size_t)RB * G::NN * G::PSQ;
-    vs = off;
-    off += sizeof(double) * (size_t)G::VST * L;
     // the pixel queue: C2 of step s reads it before the barrier after A of
     // step s+1 and C1 of step s+1 writes it after the next one: single
     // buffer; nup_1..nup_N (nup_0 = n is not stored)
@@ -959,6 +960,9 @@ struct FilterSmem {
     off = (off + 15) & ~(size_t)15;
     q4 = off;  // !FB: (theta, sigma, alpha, beta) of each record, one 16-byte access
     off += FB ? 0 : sizeof(float4) * QS;
+    off = (off + 7) & ~(size_t)7;
+    vs = off;
+    off += sizeof(double) * (size_t)G::VST * L;
     off = (off + 7) & ~(size_t)7;
     vx = off;  // vertical (min, max) of each input column, per step row
     off += sizeof(float2) * (size_t)RB * XP;
@@ -996,7 +1000,7 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
   float2* VZ = reinterpret_cast<float2*>(smraw + lay.vz);    // [RB][YP]
   const float n = (float)(w * w);
   const bool want_t2n = a.d_t2n != nullptr, want_kappa = a.d_kappa != nullptr;
-  const bool want_diag = want_t2n || want_kappa || a.d_code != nullptr;  // fabf_filter_diag
+  const bool want_diag = want_t2n || want_kappa || a.d_code != nullptr || a.d_alpha != nullptr;  // fabf_filter_diag
   const float2 kEmpty = make_float2(CUDART_INF_F, -CUDART_INF_F);
 
   for (int i = tid; i < RB * NN * PSQ; i += kThreads) Ps[i] = 0.0;  // P[0] = 0 for good
@@ -1304,7 +1308,8 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
         for (int r = 0; r < RB; ++r) {
           if (r < nr) {
             const double ui = fma((double)fin[r], invS, mcs);
-            const double uo = (Yb + r == Y0) ? 0.0 : fma((double)fout[r], invS, mcs);
+            // (only the segment's first row has no leaving sample: r = 0 of its first step)
+            const double uo = (r == 0 && Yb == Y0) ? 0.0 : fma((double)fout[r], invS, mcs);
             // d_q = ui^q - uo^q by its own recurrence d_{q+1} = (ui + uo) d_q
             // - ui uo d_{q-1} (d_0 = 0): one DMUL + one DFMA per power instead
             // of two DMULs and a DADD
@@ -1479,9 +1484,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
       // (two passes: regimes of this thread's PPT pixels first, so that one
       // shared atomic per warp and step reserves the slots of all of them)
       int regime[PPT];
+      double p_m[PPT], p_h[PPT];  // midrange, half-range in tile units (flag test and stretch)
 #pragma unroll
       for (int i = 0; i < PPT; ++i) {
         regime[i] = -1;  // -1: no record (invalid, identity or fallback)
+        p_m[i] = 0.0, p_h[i] = 1.0;
         if constexpr (FB) {
           const int pix = (px_r + i * (kThreads / TW)) * YP + px_x;
           const float2 ab = mm2(VY[pix], VZ[pix]);
@@ -1489,27 +1496,33 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
           p_be[i] = ab.y;
         }
         if (pvalid[i]) {
-          if (a.d_alpha) {
-            a.d_alpha[po[i]] = p_al[i];
-            a.d_beta[po[i]] = p_be[i];
-          }
+          // (diagnostics: alpha, beta of the pixels that get a record are stored
+          // by C2's diagnostic copy; the two rare branches store their own)
           if (p_al[i] == p_be[i]) {  // P:204, Algorithm 1 lines 4-5: g-hat = f(i) = alpha
             a.out[po[i]] = p_al[i];
+            if (a.d_alpha) {
+              a.d_alpha[po[i]] = p_al[i];
+              a.d_beta[po[i]] = p_be[i];
+            }
             if (a.d_kappa) a.d_kappa[po[i]] = 1.0f;
             if (a.d_t2n) a.d_t2n[po[i]] = 1.0f;
             if (a.d_code) a.d_code[po[i]] = (unsigned char)kCodeIdentity;
-          } else if (stretch_flagged(fma((double)p_al[i], invS, mcs), fma((double)p_be[i], invS, mcs),
-                                     a.flag_root)) {  // exact-moment fallback pass
+          } else if (const double au = fma((double)p_al[i], invS, mcs), bu = fma((double)p_be[i], invS, mcs);
+                     (p_m[i] = 0.5 * (au + bu), p_h[i] = 0.5 * (bu - au),
+                      1.0 + fabs(p_m[i]) > a.flag_root * p_h[i])) {  // stretch_flagged: exact-moment fallback pass
             const int pX = x0 + px_x, pY = Yb + px_r + i * (kThreads / TW);
             const int sw = (bimg * H + pY) * a.WS + (pX >> 5);
             if (atomicOr(&a.fb_bits[sw], 1u << (pX & 31)) == 0u) a.seg_list[atomicAdd(a.seg_count, 1)] = sw;
+            if (a.d_alpha) {
+              a.d_alpha[po[i]] = p_al[i];
+              a.d_beta[po[i]] = p_be[i];
+            }
             if constexpr (FB) {  // the fallback kernel reads alpha, beta from the plan
               a.alpha_w[po[i]] = p_al[i];
               a.beta_w[po[i]] = p_be[i];
             }
           } else {
-            float lam, t0;
-            regime[i] = range_params(p_al[i], p_be[i], p_th[i], p_sg[i], lam, t0);
+            regime[i] = regime_of(p_al[i], p_be[i], p_th[i], p_sg[i]);
           }
         }
       }
@@ -1544,11 +1557,11 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               S[q] = acc;
             }
           }
-          const double au = fma((double)p_al[i], invS, mcs), bu = fma((double)p_be[i], invS, mcs);
           const int j = (regime[i] == kRegA) ? baseA + __popc(mA[i] & lt)
                                              : QS - 1 - (baseB + __popc(mB[i] & lt));
-          nu_from_sums<N>(S, au, bu, qnu + j, QS);
-          qo[j] = (px_r + i * (kThreads / TW)) * TW + px_x;  // in-step pixel index
+          nu_from_sums_mh<N>(S, p_m[i], p_h[i], qnu + j, QS);
+          // FB: in-step pixel index (C2 looks alpha, beta up in VY / VZ); else the output index itself
+          qo[j] = FB ? (px_r + i * (kThreads / TW)) * TW + px_x : po[i];
           if constexpr (!FB) q4[j] = make_float4(p_th[i], p_sg[i], p_al[i], p_be[i]);
         }
         baseA += __popc(mA[i]);
@@ -1576,10 +1589,12 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
             const double* nu = qnu + j;  // nup_k = nu[(k - 1) * QS]
             // the record's pixel within the step: (alpha, beta) still in VY / VZ
             // (rewritten only in the next step's phase A, after C2 of this one)
-            const int pix = qo[j], pr = pix / TW, px = pix - pr * TW;
-            const int o = rowbase + pr * W + px;
+            const int pix = qo[j];
+            int o = pix;
             float th, sg, al, be;
             if constexpr (FB) {
+              const int pr = pix / TW, px = pix - pr * TW;
+              o = rowbase + pr * W + px;
               const float2 ab = mm2(VY[pr * YP + px], VZ[pr * YP + px]);
               th = __ldg(a.theta + o), sg = __ldg(a.sigma + o), al = ab.x, be = ab.y;
             } else {
@@ -1587,14 +1602,15 @@ __global__ void __launch_bounds__(kThreads, FABF_FILTER_MINB) k_filter(FilterArg
               th = rec.x, sg = rec.y, al = rec.z, be = rec.w;
             }
             int regime = kRegA;
-            if (j >= nA) {
-              float lam, t0;
-              regime = range_params(al, be, th, sg, lam, t0);
-            }
+            if (j >= nA) regime = regime_of(al, be, th, sg);
             PixelResult res = ghat_from_record<N, true>(nu, QS, th, sg, al, be, regime, a.flags, D && want_t2n, n,
                                                         s_etab, D && want_kappa);
             a.out[o] = res.g;
             if constexpr (D) {
+              if (a.d_alpha) {
+                a.d_alpha[o] = al;
+                a.d_beta[o] = be;
+              }
               if (a.d_kappa) a.d_kappa[o] = res.kappa;
               if (a.d_t2n) a.d_t2n[o] = res.t2n;
               if (a.d_code) a.d_code[o] = (unsigned char)res.code;

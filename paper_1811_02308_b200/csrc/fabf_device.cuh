@@ -313,6 +313,14 @@ enum Regime : int { kRegA = 0, kRegB = 1, kRegC = 2 };
 // a6: lambda = (beta-alpha)^2 / (2 sigma^2) (eq.(25)) and
 // theta_0 = (theta-alpha)/(beta-alpha), both rounded to fp32 (the
 // output's sensitivity to them is ~1e-5 grey), and the regime.
+// The regime alone, without the divisions (d > 0, sigma > 0): t0 < -1 <=> theta - alpha < -d,
+// t0 > 2 <=> theta - alpha > 2 d, lambda < kLambdaSmall <=> d^2 < 2 kLambdaSmall sigma^2.
+__device__ __forceinline__ int regime_of(float alpha, float beta, float theta, float sigma) {
+  const float d = beta - alpha, x = theta - alpha;
+  if (x < -d || x > 2.0f * d) return 2;  // kRegC
+  return (d * d < (float)(2.0 * kLambdaSmall) * (sigma * sigma)) ? 1 : 0;  // kRegB : kRegA
+}
+
 __device__ __forceinline__ int range_params(float alpha, float beta, float theta, float sigma,
                                             float& lam, float& t0) {
   const float d = beta - alpha;  // exact unless the range spans >2^24 ulps
@@ -393,13 +401,10 @@ __device__ __forceinline__ PixelResult ghat_from_record(const double* nup, int n
     scale_log = lam * dist * dist - 0.69314718055994530942;  // A = J here
     contract<N>(nup, ns, n, A, X, T2f, Uf, abf, A0f, X0f);
   }
-  float ratio;
-  if (!(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f)) {
-    ratio = __fdividef(X0f, A0f);
-    res.code |= kCodeGuard;
-  } else {
-    ratio = __fdividef(Uf, T2f);  // (2 ulp: the sums carry the cancellation, not the ratio)
-  }
+  // one division on the selected operands (2 ulp: the sums carry the cancellation, not the ratio)
+  const bool guard = !(flags & kFlagLiteral) && (!(T2f > 0.0f) || abf > kKappaMax * T2f);
+  if (guard) res.code |= kCodeGuard;
+  const float ratio = __fdividef(guard ? X0f : Uf, guard ? A0f : T2f);
   res.kappa = !want_kappa ? 0.0f : (T2f > 0.0f) ? abf / T2f : CUDART_INF_F;
   // T2 / n in the units of eq.(29) (J = A/2, unscaled)
   res.t2n = want_t2n ? (float)(0.5 * (double)T2f / n * exp(-scale_log)) : 0.0f;
@@ -439,10 +444,9 @@ __device__ __forceinline__ bool stretch_flagged(double au, double bu, double fla
   const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
   return 1.0 + fabs(m) > flag_root * h;
 }
+// (m, h = the pixel's midrange and half-range in tile units, as stretch_flagged forms them)
 template <int N>
-__device__ __forceinline__ void nu_from_sums(double S[N + 1], double au, double bu, double* nup,
-                                             int ns) {
-  const double m = 0.5 * (au + bu), h = 0.5 * (bu - au);
+__device__ __forceinline__ void nu_from_sums_mh(double S[N + 1], double m, double h, double* nup, int ns) {
 #pragma unroll
   for (int i = 1; i <= N; ++i) {
 #pragma unroll
@@ -462,6 +466,11 @@ __device__ __forceinline__ void nu_from_sums(double S[N + 1], double au, double 
     for (int r = k & 1; r <= k; r += 2) v = fma((double)(2 * k + 1) * leg_coef(k, r), S[r], v);
     nup[(k - 1) * ns] = v;
   }
+}
+template <int N>
+__device__ __forceinline__ void nu_from_sums(double S[N + 1], double au, double bu, double* nup,
+                                             int ns) {
+  nu_from_sums_mh<N>(S, 0.5 * (au + bu), 0.5 * (bu - au), nup, ns);
 }
 
 __device__ __forceinline__ int reflect_hi(int i, int n) { return i < n ? i : 2 * n - 1 - i; }
