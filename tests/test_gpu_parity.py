@@ -587,6 +587,30 @@ def test_texture_maps(fb, orc, kind, shape, patch):
     assert sg.min() >= 6.0 - 1e-5 and sg.max() <= 44.0 + 1e-5
 
 
+def test_texture_entry_points_refuse_bad_arguments(fb):
+    """fabf_texture_maps / fabf_filter_texture: INVALID_ARGUMENT for a patch
+    outside [0, 16] or wider than the image, non-positive map parameters,
+    sigma_hi < sigma_lo, and intermediates that overlap the input."""
+    import torch
+
+    plan = fb.Plan(1, 24, 40)
+    img = torch.rand(1, 24, 40, device="cuda") * 255
+    for bad in (dict(patch=17), dict(patch=-1), dict(patch=12), dict(mrtv_sat=0.0), dict(eps=0.0),
+                dict(sigma_lo=0.0), dict(sigma_lo=9.0, sigma_hi=8.0), dict(second_scale=0.0)):
+        with pytest.raises(fb.FabfError) as e:
+            fb.texture_maps(plan, img, **bad)
+        assert e.value.status == 1, bad
+    with pytest.raises(fb.FabfError):
+        fb.filter_texture(plan, img, 2, 3, pass1=img)
+    with pytest.raises(fb.FabfError):
+        fb.filter_texture(plan, img, 12, 3)  # window taller than the image
+    with pytest.raises(fb.FabfError):
+        fb.filter_texture(plan, img, 2, 3, rho_sharpen=12)
+    out = fb.filter_texture(plan, img, 2, 3)  # the plan still works afterwards
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+
+
 @pytest.mark.parametrize("kind,shape,rho,N,rs", [
     ("texture", (1, 150, 170), 5, 5, 3), ("rect", (2, 90, 110), 3, 6, 3), ("voronoi", (1, 128, 96), 10, 8, 5)])
 def test_texture_application(fb, orc, kind, shape, rho, N, rs):
