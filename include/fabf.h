@@ -206,6 +206,17 @@ fabf_status_t fabf_filter_texture(fabf_plan_t plan, const float* img, int rho, i
                                   int rho_sharpen, const fabf_sharpen_t* sprm, float* out, float* pass1,
                                   float* pass2, void* stream);
 
+/* The same three passes with the CALLER's sigma map (device, batch x height x
+ * width fp32, > 0, 16-byte aligned; pass 1 uses it as it is, pass 2 scaled by
+ * second_scale).  This is how the paper treats colour images (P:848, P:853:
+ * mRTV and sigma "on a grayscale version of the color image", the channels
+ * then filtered one by one): fabf_texture_maps on the grey plane, that map
+ * repeated for every channel plane of a planar batch, then this call.         */
+fabf_status_t fabf_filter_texture_map(fabf_plan_t plan, const float* img, const float* sigma_map,
+                                      float second_scale, int rho, int N, int rho_sharpen,
+                                      const fabf_sharpen_t* sprm, float* out, float* pass1, float* pass2,
+                                      void* stream);
+
 /* The baseline the paper compares with (NEXT-4): Mozerov & van de Weijer's
  * uniform-prior filter with Delta = 0 (Fig.3) -- eq.(29) at
  * N = 0 fitted on [f(i), 2 fbar(i) - f(i)] (fbar = the box mean over the same

@@ -21,6 +21,7 @@ from .fabf import (  # noqa: F401
     sharpen_maps,
     SHARPEN_DEFAULTS,
     filter_texture,
+    filter_texture_map,
     texture_maps,
     TEXTURE_DEFAULTS,
     filter_profile,

@@ -2277,6 +2277,14 @@ __global__ void __launch_bounds__(kThreads) k_interleave(const float* __restrict
   }
 }
 
+// sigma2 = scale * sigma (the texture application's second pass on a caller's map)
+__global__ void __launch_bounds__(kThreads) k_scale(const float* __restrict__ x, float* __restrict__ y, float scale,
+                                                     long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x)
+    y[t] = scale * x[t];
+}
+
 // ============================================================================
 // FABF_FLAG_DEBUG: device-side check of the preconditions (include/fabf.h):
 // f, theta finite, sigma finite and > 0.  Counts violations of the pixels
@@ -3261,47 +3269,78 @@ fabf_status_t fabf_texture_maps(fabf_plan_t plan, const float* img, const fabf_t
   return texture_maps_impl(p, img, prm, sigma, nullptr, mrtv, (cudaStream_t)stream);
 }
 
-fabf_status_t fabf_filter_texture(fabf_plan_t plan, const float* img, int rho, int N, const fabf_texture_t* tprm,
-                                  int rho_sharpen, const fabf_sharpen_t* sprm, float* out, float* pass1,
-                                  float* pass2, void* stream) {
-  // Algorithm 1 three times -- theta = f with the mRTV sigma map,
-  // again on the result with sigma scaled by second_scale (the same map), then
-  // the sharpening rule of P:620-630 on that
-  Plan* p = reinterpret_cast<Plan*>(plan);
+namespace {
+// Algorithm 1 three times -- theta = f with the sigma map, again on
+// the result with sigma scaled by second_scale (the same map), then the
+// sharpening rule of P:620-630 on that.  The map comes from k_texture_maps
+// (tprm) or from the caller (sigma_map, second_scale).
+fabf_status_t texture_passes(Plan* p, const float* img, int rho, int N, const fabf_texture_t* tprm,
+                             const float* sigma_map, float second_scale, int rho_sharpen,
+                             const fabf_sharpen_t* sprm, float* out, float* pass1, float* pass2, cudaStream_t st) {
   fabf_status_t s = validate_common(p, rho);
   if (s != FABF_OK) return s;
-  if (!img || !out || !tprm || !sprm) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!img || !out || !sprm || (!tprm && !sigma_map)) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
   const size_t px = (size_t)p->B * p->H * p->W, bytes = px * sizeof(float);
   if ((pass1 && (overlaps(pass1, bytes, img, bytes) || overlaps(pass1, bytes, out, bytes))) ||
       (pass2 && (overlaps(pass2, bytes, img, bytes) || overlaps(pass2, bytes, out, bytes))) ||
       (pass1 && pass2 && overlaps(pass1, bytes, pass2, bytes)))
     return fail(FABF_ERR_INVALID_ARGUMENT, "pass1 / pass2 overlap another buffer");
+  if (sigma_map && (!(second_scale > 0.0f) || !aligned16(sigma_map) || overlaps(sigma_map, bytes, out, bytes) ||
+                    (pass1 && overlaps(sigma_map, bytes, pass1, bytes)) ||
+                    (pass2 && overlaps(sigma_map, bytes, pass2, bytes))))
+    return fail(FABF_ERR_INVALID_ARGUMENT, "sigma map: second_scale > 0, 16-byte aligned, no overlap with an output");
   s = ensure_staging(p);
   if (s != FABF_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
   const size_t pitch = staging_pitch(px);
   float* g1 = pass1 ? pass1 : p->h_in;
   float* g2 = pass2 ? pass2 : p->h_out;
   float* pa = p->h_in + pitch;      // sigma, then theta of the sharpening pass
   float* pb = p->h_in + 2 * pitch;  // second_scale * sigma, then sigma of the sharpening pass
   g_launches = 0;
-  s = texture_maps_impl(p, img, tprm, pa, pb, nullptr, st);
-  if (s != FABF_OK) return s;
+  const float* sg1 = pa;
+  if (sigma_map) {
+    sg1 = sigma_map;
+    const int grid = (int)std::min<long long>(148LL * 8, ((long long)px + kThreads - 1) / kThreads);
+    k_scale<<<grid, kThreads, 0, st>>>(sigma_map, pb, second_scale, (long long)px);
+    FABF_CUDA(cudaGetLastError(), "k_scale launch");
+    ++g_launches;
+  } else {
+    s = texture_maps_impl(p, img, tprm, pa, pb, nullptr, st);
+    if (s != FABF_OK) return s;
+  }
   int total = g_launches;
-  s = filter_impl(p, img, img, pa, rho, N, g1, nullptr, st);
+  s = filter_impl(p, img, img, sg1, rho, N, g1, nullptr, st);
   if (s != FABF_OK) return s;
   total += p->launches;
   s = filter_impl(p, g1, g1, pb, rho, N, g2, nullptr, st);
   if (s != FABF_OK) return s;
   total += p->launches;
   g_launches = 0;
-  s = fabf_sharpen_maps(plan, g2, rho_sharpen, sprm, pa, pb, stream);
+  s = fabf_sharpen_maps(p, g2, rho_sharpen, sprm, pa, pb, st);
   if (s != FABF_OK) return s;
   total += g_launches;
   s = filter_impl(p, g2, pa, pb, rho_sharpen, N, out, nullptr, st);
   if (s != FABF_OK) return s;
   p->launches += total;
   return FABF_OK;
+}
+}  // namespace
+
+fabf_status_t fabf_filter_texture(fabf_plan_t plan, const float* img, int rho, int N, const fabf_texture_t* tprm,
+                                  int rho_sharpen, const fabf_sharpen_t* sprm, float* out, float* pass1,
+                                  float* pass2, void* stream) {
+  if (!tprm) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  return texture_passes(reinterpret_cast<Plan*>(plan), img, rho, N, tprm, nullptr, 0.0f, rho_sharpen, sprm, out,
+                        pass1, pass2, (cudaStream_t)stream);
+}
+
+fabf_status_t fabf_filter_texture_map(fabf_plan_t plan, const float* img, const float* sigma_map,
+                                      float second_scale, int rho, int N, int rho_sharpen,
+                                      const fabf_sharpen_t* sprm, float* out, float* pass1, float* pass2,
+                                      void* stream) {
+  if (!sigma_map) return fail(FABF_ERR_INVALID_ARGUMENT, "NULL pointer");
+  return texture_passes(reinterpret_cast<Plan*>(plan), img, rho, N, nullptr, sigma_map, second_scale, rho_sharpen,
+                        sprm, out, pass1, pass2, (cudaStream_t)stream);
 }
 
 fabf_status_t fabf_filter_interleaved(fabf_plan_t plan, const float* img, const float* theta,

@@ -88,6 +88,9 @@ def lib():
                 L.fabf_filter_texture.argtypes = [P, P, i, i, ctypes.POINTER(_Texture), i, ctypes.POINTER(_Sharpen),
                                                   P, P, P, P]
                 L.fabf_filter_texture.restype = ctypes.c_int
+                L.fabf_filter_texture_map.argtypes = [P, P, P, ctypes.c_float, i, i, i, ctypes.POINTER(_Sharpen),
+                                                      P, P, P, P]
+                L.fabf_filter_texture_map.restype = ctypes.c_int
             if hasattr(L, "fabf_filter_gauss"):
                 L.fabf_filter_gauss.argtypes = [P, P, P, P, i, i, P, P]
                 L.fabf_filter_gauss.restype = ctypes.c_int
@@ -400,6 +403,24 @@ def filter_texture(plan: Plan, img, rho: int, N: int, texture=None, sharpen=None
                                      ctypes.byref(sp), _dev_ptr(out, "out", plan),
                                      None if pass1 is None else _dev_ptr(pass1, "pass1", plan),
                                      None if pass2 is None else _dev_ptr(pass2, "pass2", plan), _stream_ptr(stream)))
+    return out
+
+
+def filter_texture_map(plan: Plan, img, sigma_map, rho: int, N: int, second_scale: float = 0.8, sharpen=None,
+                       rho_sharpen=None, out=None, pass1=None, pass2=None, stream=None):
+    """fabf_filter_texture_map: the three passes with the caller's sigma map (the
+    paper's colour procedure: the map of the grey image for every channel plane)."""
+    import torch
+
+    out = torch.empty_like(img) if out is None else out
+    sp = _sharpen_params(sharpen or {})
+    rs = int(rho if rho_sharpen is None else rho_sharpen)
+    _check(lib().fabf_filter_texture_map(plan.handle, _dev_ptr(img, "img", plan), _dev_ptr(sigma_map, "sigma_map", plan),
+                                         float(second_scale), int(rho), int(N), rs, ctypes.byref(sp),
+                                         _dev_ptr(out, "out", plan),
+                                         None if pass1 is None else _dev_ptr(pass1, "pass1", plan),
+                                         None if pass2 is None else _dev_ptr(pass2, "pass2", plan),
+                                         _stream_ptr(stream)))
     return out
 
 

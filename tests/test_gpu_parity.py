@@ -653,6 +653,44 @@ def test_texture_application(fb, orc, kind, shape, rho, N, rs):
     assert np.quantile(d, 0.999) <= TOL_GREY, f"end to end p99.9 = {np.quantile(d, 0.999)} grey, max {d.max()}"
 
 
+def test_texture_application_colour_with_grey_map(fb, orc):
+    """The paper's colour procedure: mRTV / sigma on the grey
+    version, the channels filtered one by one with that map
+    (fabf_filter_texture_map).  Stage by stage against the oracle on the
+    device's own intermediates, and the map equals the oracle's map of the grey
+    image."""
+    import torch
+
+    rho, N, rs = 4, 5, 3
+    w = workloads.random_case(3, 90, 104, seed=99, kind="texture", rho=rho, N=N)  # three channel planes
+    grey = w.img.mean(axis=0, keepdims=True).astype(np.float32)
+    tp = dict(patch=2, sigma_lo=7.0, sigma_hi=32.0, mrtv_sat=10.0, eps=1e-3)
+    sp = dict(log_scale=1.0, sigma_lo=9.0, sigma_hi=25.0, log_sat=15.0)
+    sg_grey, _ = fb.texture_maps(fb.Plan(1, 90, 104), _dev(grey), **tp)
+    assert np.max(np.abs(sg_grey.cpu().numpy() - orc.texture_maps(grey, **tp)[1])) <= 1e-4
+    sg = sg_grey.repeat(3, 1, 1).contiguous()
+    plan = fb.Plan(3, 90, 104)
+    img = _dev(w.img)
+    g1, g2 = torch.empty_like(img), torch.empty_like(img)
+    out = fb.filter_texture_map(plan, img, sg, rho, N, second_scale=0.8, sharpen=sp, rho_sharpen=rs, pass1=g1, pass2=g2)
+    torch.cuda.synchronize()
+    sgh, g1, g2, out = sg.cpu().numpy(), g1.cpu().numpy(), g2.cpu().numpy(), out.cpu().numpy()
+    sc = grey_scale(w.img)
+    mx, nbad, _ = compare_guarded(g1, orc.fast(w.img, w.img, sgh, rho, N), sc)
+    assert nbad == 0, f"pass 1: max |delta| = {mx} grey"
+    mx, nbad, _ = compare_guarded(g2, orc.fast(g1, g1, (np.float32(0.8) * sgh).astype(np.float32), rho, N), sc)
+    assert nbad == 0, f"pass 2: max |delta| = {mx} grey"
+    th3, sg3 = fb.sharpen_maps(plan, _dev(g2), rs, **sp)
+    torch.cuda.synchronize()
+    mx, nbad, _ = compare_guarded(out, orc.fast(g2, th3.cpu().numpy(), sg3.cpu().numpy(), rs, N), sc)
+    assert nbad == 0, f"pass 3: max |delta| = {mx} grey"
+    ref = orc.texture_pipeline(w.img, rho, N, texture=dict(second_scale=0.8), sharpen=sp, rho_sharpen=rs, sigma=sgh)
+    d = np.abs(out.astype(np.float64) - ref["out"]) / sc
+    assert np.quantile(d, 0.999) <= TOL_GREY, f"end to end p99.9 = {np.quantile(d, 0.999)} grey, max {d.max()}"
+    with pytest.raises(fb.FabfError):
+        fb.filter_texture_map(plan, img, sg, rho, N, second_scale=0.0)
+
+
 @pytest.mark.parametrize("kind,shape,rho,N", [
     ("voronoi", (1, 96, 130), 3, 5), ("texture", (2, 70, 81), 1, 8), ("rect", (1, 100, 100), 5, 2),
     ("float", (1, 80, 90), 3, 6), ("flat", (1, 40, 40), 2, 5), ("voronoi", (1, 130, 150), 10, 5),
