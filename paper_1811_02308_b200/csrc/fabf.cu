@@ -812,12 +812,14 @@ __global__ void __launch_bounds__(kThreads) k_bounds2(const float* __restrict__ 
       vhgw_regs<SEGV>([&](int i) { return in[i * (kB2P / 2)]; }, w, res);
       if (x < W) {
         float2 m = make_float2(CUDART_INF_F, -CUDART_INF_F);
+        // one base per plane, 32-bit row offsets (a tile's rows span < 2^31 elements)
+        float* __restrict__ pa = amin + plane + (size_t)(y0 + ys) * W + x;
+        float* __restrict__ pb = bmax + plane + (size_t)(y0 + ys) * W + x;
 #pragma unroll
         for (int o = 0; o < SEGV; ++o) {
           if (ys + o < ny) {
-            const size_t off = plane + (size_t)(y0 + ys + o) * W + x;
-            amin[off] = res[o].x;
-            bmax[off] = res[o].y;
+            pa[o * W] = res[o].x;
+            pb[o * W] = res[o].y;
             m = mm2(m, res[o]);
           }
         }
